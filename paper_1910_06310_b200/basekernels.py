@@ -1,0 +1,148 @@
+"""Pluggable base kernels, mirroring ``mgksolver.basekernels``.
+
+The classes keep the reference names, constructor arguments, ``flop_count``
+(the cost model's X contribution) and ``with_role`` (reference
+``basekernels.py:28-261``).  They carry no arithmetic on the host: each one
+lowers to a small descriptor (``device_descriptor``) that the CUDA solver
+evaluates in-kernel for every fused contribution.  Variants the device does
+not implement raise ``NotImplementedError`` at lowering time rather than
+silently falling back to the CPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+# descriptor kind codes shared with csrc/mgk_types.h
+K_CONST1, K_DELTA, K_SE, K_POLY = 0, 1, 2, 3
+MAX_POLY = 8
+
+
+class KernelShapeError(ValueError):
+    """Label payload does not match what the kernel variant expects."""
+
+
+class KernelRangeError(ValueError):
+    """Kernel evaluated outside its admissible range in validation mode."""
+
+
+class BaseKernel:
+    role: str = "edge"
+    flop_count: int = 1
+
+    def with_role(self, role: str) -> "BaseKernel":
+        if role not in ("vertex", "edge"):
+            raise ValueError(f"unknown kernel role {role!r}")
+        self.role = role
+        return self
+
+    def device_descriptor(self) -> tuple[int, list[float]]:
+        raise NotImplementedError(f"{type(self).__name__} has no device lowering yet")
+
+
+@dataclass
+class ConstantOne(BaseKernel):
+    """kappa = 1 (basekernels.py:60-70)."""
+
+    flop_count: int = 0
+
+    def device_descriptor(self):
+        return K_CONST1, []
+
+
+@dataclass
+class KroneckerDelta(BaseKernel):
+    """1 if labels equal (all components for vectors) else h (basekernels.py:73-95)."""
+
+    h: float
+    flop_count: int = 1
+
+    def __post_init__(self):
+        if not (0 < self.h <= 1):
+            raise ValueError(f"delta baseline h must be in (0, 1], got {self.h}")
+
+    def device_descriptor(self):
+        return K_DELTA, [float(self.h)]
+
+
+@dataclass
+class SquareExponential(BaseKernel):
+    """exp(-alpha |a-b|^2) (basekernels.py:98-125)."""
+
+    alpha: float
+    flop_count: int = 4
+
+    def __post_init__(self):
+        if self.alpha <= 0:
+            raise ValueError("alpha must be positive")
+
+    def device_descriptor(self):
+        return K_SE, [float(self.alpha)]
+
+
+@dataclass
+class CompactPolynomial(BaseKernel):
+    """Horner on |a-b| of scalar labels, clamped to [0,1] (basekernels.py:128-172)."""
+
+    coeffs: Sequence[float]
+    validate: bool = False
+
+    def __post_init__(self):
+        self.coeffs = tuple(float(c) for c in self.coeffs)
+        if not self.coeffs:
+            raise ValueError("need at least one coefficient")
+        self.flop_count = max(len(self.coeffs) - 1, 1)
+
+    def device_descriptor(self):
+        if self.validate:
+            raise NotImplementedError("CompactPolynomial(validate=True) has no device lowering")
+        if len(self.coeffs) > MAX_POLY:
+            raise NotImplementedError(f"at most {MAX_POLY} polynomial coefficients on device")
+        return K_POLY, list(self.coeffs)
+
+
+@dataclass
+class ProductComposite(BaseKernel):
+    """Component-wise product (basekernels.py:175-211); device lowering pending."""
+
+    components: Sequence[BaseKernel]
+
+    def __post_init__(self):
+        self.components = tuple(self.components)
+        self.flop_count = sum(k.flop_count for k in self.components) + max(len(self.components) - 1, 0)
+
+
+@dataclass
+class RConvolution(BaseKernel):
+    """Sum over component pairs (basekernels.py:214-244); device lowering pending."""
+
+    inner: BaseKernel
+
+    def __post_init__(self):
+        self.flop_count = self.inner.flop_count + 1
+
+
+def kernel_from_spec(spec: str) -> BaseKernel:
+    """``const1 | delta:H | se:ALPHA | poly:C0,C1,...`` (basekernels.py:247-261)."""
+    head, _, rest = spec.partition(":")
+    if head == "const1":
+        return ConstantOne()
+    if head == "delta":
+        return KroneckerDelta(h=float(rest))
+    if head == "se":
+        return SquareExponential(alpha=float(rest))
+    if head == "poly":
+        return CompactPolynomial(coeffs=[float(c) for c in rest.split(",")])
+    raise ValueError(f"unknown kernel spec {spec!r}")
+
+
+def as_kernel(k, role: str):
+    """Accept a BaseKernel, a SPEC string or None."""
+    if k is None:
+        return None
+    if isinstance(k, str):
+        k = kernel_from_spec(k)
+    if not isinstance(k, BaseKernel):
+        raise TypeError(f"expected a BaseKernel or spec string, got {type(k).__name__}")
+    return k.with_role(role)
