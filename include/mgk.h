@@ -1,0 +1,119 @@
+/* mgk.h -- C-ABI of the B200 marginalized-graph-kernel solver (libmgk.so).
+ *
+ * This is the drop-in boundary for the reference's array bindings
+ * (pkg/bindings/src/mgkbind) and its core facade (pkg/src/mgksolver):
+ * plain pointers and sizes, no torch or numpy types.  Each entry point names
+ * the reference interface it replaces.  Return codes: 0 = ok, < 0 = error
+ * class (MGK_E_*); mgk_last_error() returns the thread-local message, whose
+ * text follows the reference's exceptions (graphs.py:161-199, product.py:
+ * 153-178, solver.py:226-231).  The library copies what it needs and never
+ * retains caller pointers after a call returns.  A context is bound to one
+ * CUDA device; calls on one context are serialised by the caller.
+ */
+#ifndef MGK_H
+#define MGK_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mgk_ctx mgk_ctx;
+
+enum {
+  MGK_OK = 0,
+  MGK_E_INVALID = -1,   /* ValueError: invalid graph / argument (graphs.py:161-199, solver.py:226-231) */
+  MGK_E_SHAPE = -2,     /* KernelShapeError (basekernels.py:14-15, product.py:153-178) */
+  MGK_E_CUDA = -3,      /* CUDA runtime failure (no CPU fallback exists) */
+  MGK_E_UNSUPPORTED = -4, /* kernel variant without a device lowering */
+  MGK_E_STATE = -5      /* call order (e.g. solve before upload) */
+};
+
+/* label kinds (graphs.py:126-146) */
+enum { MGK_LABEL_NONE = 0, MGK_LABEL_CATEGORICAL = 1, MGK_LABEL_VECTOR = 2 };
+/* reorder methods (solver.py:209, 249-259) */
+enum { MGK_REORDER_NONE = 0, MGK_REORDER_PBR = 1 };
+
+/* Version string of the library build. */
+const char* mgk_version(void);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* mgk_last_error(void);
+
+/* Create a context on CUDA device `device` (replaces the per-call
+ * `python -m mgksolver` subprocess of marshal.py:150-155). */
+int mgk_ctx_create(mgk_ctx** out, int device);
+int mgk_ctx_destroy(mgk_ctx* ctx);
+
+/* Upload a dataset of N graphs in packed form (replaces write_graph_json +
+ * load_graph, marshal.py:87-115 / graphio.py:115-180, and the LabeledGraph
+ * list passed to compute_gram, gram.py:57).
+ *   node_off[N+1], edge_off[N+1]: prefix offsets into the node / edge arrays;
+ *   ei, ej: endpoints local to their graph (stored once per undirected edge);
+ *   w: edge weights; p, q: start / stop probabilities per node;
+ *   node_labels: int64[sum n] (categorical) or double[sum n * nl_dim] (vector);
+ *   edge_labels: int64[sum E] or double[sum E * el_dim].
+ * Validation follows validate_graph (graphs.py:161-199); the first invalid
+ * graph fails the call with "graph <g> invalid: <violations>". */
+int mgk_upload(mgk_ctx* ctx, int32_t N, const int64_t* node_off, const int64_t* edge_off, const int32_t* ei,
+               const int32_t* ej, const double* w, const double* p, const double* q, int nl_kind, int nl_dim,
+               const void* node_labels, int el_kind, int el_dim, const void* edge_labels);
+
+/* Base kernels by the reference SPEC grammar `const1 | delta:H | se:A | poly:c0,c1,..`
+ * (basekernels.py:247-261); NULL or "" means None (vertex: all-ones
+ * similarity, product.py:172; edge: kappa = 1, product.py:74-79). */
+int mgk_set_kernels(mgk_ctx* ctx, const char* vertex_spec, const char* edge_spec);
+
+/* Per-graph partition-based reordering on the device (pbr_reorder,
+ * reorder.py:361-404), same seed for every graph (solver.py:236-237).
+ * Writes forward maps (old -> new) into perms_out[sum n] when non-NULL.  With
+ * apply != 0 the dataset is relabelled (apply_permutation, reorder.py:86-109)
+ * and its octiles rebuilt. */
+int mgk_reorder(mgk_ctx* ctx, int method, uint64_t seed, int apply, int64_t* perms_out);
+
+/* Octiles of graph g as built on the device (build_tiles, tiles.py:85-127).
+ * Call with rc_out == NULL to get *ntiles and *nnz; then pass buffers of
+ * 2*ntiles int32 (row, col), ntiles uint64 bitmaps, nnz float values. */
+int mgk_tiles(mgk_ctx* ctx, int32_t g, int32_t* ntiles, int32_t* nnz, int32_t* rc_out, uint64_t* bitmap_out,
+              float* w_out);
+
+/* Degree vector d_i = sum_j w_ij + q_i of graph g (degree_vector, graphs.py:202-214). */
+int mgk_degrees(mgk_ctx* ctx, int32_t g, double* d_out);
+
+/* All-pairs Gram matrix (compute_gram, gram.py:57-95): K[N*N] row-major,
+ * mirrored, NaN where the pair did not converge; iters[N*N], conv[N*N].
+ * Any output may be NULL (the result then stays on the device; used by the
+ * device-resident benchmark).  max_iter 0 -> 10*n*m (solver.py:87). */
+int mgk_gram(mgk_ctx* ctx, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv);
+
+/* Shard of the Gram pairs for multi-GPU runs: this context solves the pairs
+ * whose cost-ordered id is congruent to rank modulo world, writing compact
+ * per-pair results in that order (value, iterations, converged).  *npairs_out
+ * receives the shard length. */
+int mgk_gram_shard(mgk_ctx* ctx, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
+                   double* value, int32_t* iters, uint8_t* conv);
+
+/* Scatter gathered shard results into the Gram matrix (mirrored, NaN where
+ * not converged).  values/iters/conv hold world shards concatenated in rank
+ * order with the lengths mgk_gram_shard reported. */
+int mgk_gram_assemble(mgk_ctx* ctx, int world, const int64_t* shard_len, const double* values, const int32_t* iters,
+                      const uint8_t* conv, double* K, int32_t* K_iters, uint8_t* K_conv);
+
+/* Batch of explicit pairs (the per-pair `kernel` of solver.py:212-246 without
+ * reordering): value[k], iters[k], residual[k], conv[k]; nodewise (nullable)
+ * receives the n_a x m_b float64 field of every pair back to back. */
+int mgk_pairs(mgk_ctx* ctx, int64_t npairs, const int32_t* a, const int32_t* b, double tol, int64_t max_iter,
+              double* value, int32_t* iters, double* residual, uint8_t* conv, double* nodewise);
+
+/* Single pair convenience wrapper of mgk_pairs (mgkbind.kernel, __init__.py:41-67). */
+int mgk_kernel(mgk_ctx* ctx, int32_t a, int32_t b, double tol, int64_t max_iter, double* value, double* nodewise,
+               int32_t* iters, double* residual, uint8_t* conv);
+
+/* Device time (ms, CUDA events on the solver stream) and the number of
+ * kernel launches of the last solve call. */
+int mgk_last_timing(mgk_ctx* ctx, double* solve_ms, int32_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGK_H */

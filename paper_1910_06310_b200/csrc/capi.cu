@@ -1,0 +1,935 @@
+// libmgk C-ABI: context, dataset upload/validation, label lowering, device
+// preprocessing (octiles, degrees, PBR) and solver dispatch.  See include/mgk.h.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/mgk.h"
+#include "mgk_internal.h"
+#include "pbr.h"
+
+using namespace mgk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[4096];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) return fail(MGK_E_CUDA, "CUDA error %s at %s:%d: %s", #x, __FILE__, \
+                                       __LINE__, cudaGetErrorString(e_));                    \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+  }
+  cudaError_t alloc(size_t count) {
+    if (count <= n && ptr) return cudaSuccess;
+    release();
+    n = count;
+    return cudaMalloc(&ptr, std::max<size_t>(count, 1) * sizeof(T));
+  }
+  cudaError_t upload(const std::vector<T>& v, cudaStream_t s) {
+    cudaError_t e = alloc(v.size());
+    if (e != cudaSuccess || v.empty()) return e;
+    return cudaMemcpyAsync(ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+  }
+};
+
+struct Spec {
+  int kind = KK_NONE;  // KK_NONE == None
+  double h = 1.0, alpha = 1.0;
+  std::vector<double> coef;
+};
+
+int parse_spec(const char* s, Spec& out) {
+  out = Spec();
+  if (!s || !*s) return MGK_OK;
+  std::string str(s);
+  auto colon = str.find(':');
+  std::string head = str.substr(0, colon);
+  std::string rest = colon == std::string::npos ? "" : str.substr(colon + 1);
+  try {
+    if (head == "const1") {
+      out.kind = KK_CONST1;
+    } else if (head == "delta") {
+      out.kind = KK_DELTA;
+      out.h = std::stod(rest);
+      if (!(out.h > 0 && out.h <= 1)) return fail(MGK_E_INVALID, "delta baseline h must be in (0, 1], got %g", out.h);
+    } else if (head == "se") {
+      out.kind = KK_SE;
+      out.alpha = std::stod(rest);
+      if (!(out.alpha > 0)) return fail(MGK_E_INVALID, "alpha must be positive");
+    } else if (head == "poly") {
+      out.kind = KK_POLY;
+      size_t pos = 0;
+      while (pos <= rest.size()) {
+        size_t c = rest.find(',', pos);
+        out.coef.push_back(std::stod(rest.substr(pos, c == std::string::npos ? std::string::npos : c - pos)));
+        if (c == std::string::npos) break;
+        pos = c + 1;
+      }
+      if (out.coef.empty()) return fail(MGK_E_INVALID, "need at least one coefficient");
+      if ((int)out.coef.size() > kMaxPoly)
+        return fail(MGK_E_UNSUPPORTED, "at most %d polynomial coefficients on device", kMaxPoly);
+    } else {
+      return fail(MGK_E_INVALID, "unknown kernel spec '%s'", s);
+    }
+  } catch (...) {
+    return fail(MGK_E_INVALID, "unknown kernel spec '%s'", s);
+  }
+  return MGK_OK;
+}
+
+KernelDesc to_desc(const Spec& s) {
+  KernelDesc d{};
+  d.kind = s.kind;
+  d.h = (float)s.h;
+  d.alpha = (float)s.alpha;
+  d.se_scale = (float)std::sqrt(s.alpha * 1.4426950408889634);
+  d.ncoef = (int)s.coef.size();
+  for (int i = 0; i < d.ncoef; ++i) d.coef[i] = (float)s.coef[i];
+  return d;
+}
+
+// Labels lowered for the device according to the kernel that reads them.
+struct Lowered {
+  int kind = LK_NONE;
+  int dim = 0;
+  std::vector<float> data;
+};
+
+int lower_labels(int kind, int dim, const std::vector<int64_t>& cat, const std::vector<double>& vec, size_t count,
+                 const Spec& k, Lowered& out, const char* what) {
+  out = Lowered();
+  if (kind == LK_NONE || k.kind == KK_NONE || k.kind == KK_CONST1) return MGK_OK;
+  if (k.kind == KK_DELTA) {
+    // equality classes -> dense ids: exact for int64 tokens and float vectors alike
+    out.kind = LK_CAT;
+    out.dim = 1;
+    out.data.resize(count);
+    if (kind == LK_CAT) {
+      std::map<int64_t, int32_t> ids;
+      for (size_t i = 0; i < count; ++i) {
+        auto it = ids.emplace(cat[i], (int32_t)ids.size()).first;
+        int32_t v = it->second;
+        memcpy(&out.data[i], &v, 4);
+      }
+    } else {
+      std::map<std::vector<double>, int32_t> ids;
+      for (size_t i = 0; i < count; ++i) {
+        std::vector<double> key(vec.begin() + i * dim, vec.begin() + (i + 1) * dim);
+        for (double& x : key)
+          if (x == 0.0) x = 0.0;  // -0.0 == 0.0 (numpy ==)
+        auto it = ids.emplace(key, (int32_t)ids.size()).first;
+        int32_t v = it->second;
+        memcpy(&out.data[i], &v, 4);
+      }
+    }
+    return MGK_OK;
+  }
+  if (kind == LK_CAT) dim = 1;
+  if (k.kind == KK_POLY && dim != 1)
+    return fail(MGK_E_SHAPE, "polynomial kernel expects scalar labels");
+  if (dim > kMaxLabelDim) return fail(MGK_E_UNSUPPORTED, "%s label dimension %d > %d", what, dim, kMaxLabelDim);
+  double scale = k.kind == KK_SE ? std::sqrt(k.alpha * 1.4426950408889634) : 1.0;
+  out.kind = LK_VEC;
+  out.dim = dim;
+  out.data.resize(count * dim);
+  for (size_t i = 0; i < count * dim; ++i) out.data[i] = (float)((kind == LK_CAT ? (double)cat[i] : vec[i]) * scale);
+  return MGK_OK;
+}
+
+}  // namespace
+
+struct mgk_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int last_launches = 0;
+  // host copy of the dataset
+  int32_t G = 0;
+  std::vector<int64_t> node_off, edge_off;
+  std::vector<int32_t> ei, ej;
+  std::vector<double> w, p, q;
+  int nl_kind = 0, nl_dim = 0, el_kind = 0, el_dim = 0;
+  std::vector<int64_t> nl_cat, el_cat;
+  std::vector<double> nl_vec, el_vec;
+  bool uploaded = false;
+  // kernels
+  Spec vspec, espec;
+  bool prepared = false;
+  // device dataset
+  std::vector<GraphDesc> graphs;  // host mirror after preprocessing
+  int64_t total_tiles = 0;
+  DBuf<GraphDesc> d_graphs;
+  DBuf<float> d_p, d_q, d_vlabel, d_ew, d_elabel, d_nzw, d_nzlabel;
+  DBuf<double> d_q64, d_deg;
+  DBuf<int32_t> d_ei, d_ej, d_egraph, d_ngraph, d_trow, d_segcount, d_segcursor, d_segntiles, d_seggraph, d_segrow;
+  DBuf<int64_t> d_gseg, d_segstart, d_segtile;
+  DBuf<uint64_t> d_keys, d_keys2;
+  DBuf<Octile> d_tiles;
+  DatasetDev ds{};
+  KernelDesc vk{}, ek{};
+  // solver buffers
+  DBuf<unsigned long long> d_queue;
+  DBuf<int32_t> d_list_a, d_list_b, d_list_c;
+  DBuf<double> d_K, d_value;
+  DBuf<int32_t> d_Kit, d_iters;
+  DBuf<uint8_t> d_Kconv, d_conv;
+  DBuf<float> d_resid, d_scratch, d_nodewise;
+  DBuf<int64_t> d_nwoff;
+};
+
+extern "C" {
+
+const char* mgk_version(void) { return "mgk-b200 0.1.0 (sm_100a)"; }
+
+const char* mgk_last_error(void) { return g_err.c_str(); }
+
+int mgk_ctx_create(mgk_ctx** out, int device) {
+  if (!out) return fail(MGK_E_INVALID, "null output pointer");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(MGK_E_CUDA, "no CUDA device available (%s); libmgk has no CPU fallback",
+                e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+  if (device < 0 || device >= count) return fail(MGK_E_INVALID, "device %d out of range (%d devices)", device, count);
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new mgk_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreate(&c->ev0));
+  CUDA_TRY(cudaEventCreate(&c->ev1));
+  *out = c;
+  return MGK_OK;
+}
+
+int mgk_ctx_destroy(mgk_ctx* ctx) {
+  if (!ctx) return MGK_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaEventDestroy(ctx->ev0);
+  cudaEventDestroy(ctx->ev1);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return MGK_OK;
+}
+
+// validate_graph (graphs.py:161-199) for graph g; returns the joined violations
+static std::string validate_one(const mgk_ctx* c, int g) {
+  std::vector<std::string> v;
+  int64_t n0 = c->node_off[g], n = c->node_off[g + 1] - n0;
+  int64_t e0 = c->edge_off[g], ne = c->edge_off[g + 1] - e0;
+  char buf[256];
+  if (n <= 0) v.push_back("node count must be positive");
+  for (int64_t k = 0; k < n; ++k)
+    if (c->p[n0 + k] < 0) {
+      snprintf(buf, sizeof buf, "starting probability must be >= 0 at node %lld", (long long)k);
+      v.push_back(buf);
+    }
+  for (int64_t k = 0; k < n; ++k) {
+    double qq = c->q[n0 + k];
+    if (!(qq > 0 && qq <= 1)) {
+      snprintf(buf, sizeof buf, "stopping probability must be %s at node %lld", qq <= 0 ? "> 0" : "<= 1",
+               (long long)k);
+      v.push_back(buf);
+    }
+  }
+  for (int64_t k = 0; k < ne; ++k) {
+    int a = c->ei[e0 + k], b = c->ej[e0 + k];
+    if (a < 0 || a >= n || b < 0 || b >= n) {
+      snprintf(buf, sizeof buf, "edge (%d,%d) references unknown node", a, b);
+      v.push_back(buf);
+    }
+  }
+  for (int64_t k = 0; k < ne; ++k)
+    if (c->ei[e0 + k] == c->ej[e0 + k]) {
+      snprintf(buf, sizeof buf, "self-loop at node %d", c->ei[e0 + k]);
+      v.push_back(buf);
+    }
+  for (int64_t k = 0; k < ne; ++k)
+    if (!(c->w[e0 + k] > 0)) {
+      snprintf(buf, sizeof buf, "edge weight must be > 0 at edge %lld", (long long)k);
+      v.push_back(buf);
+    }
+  std::set<std::pair<int, int>> seen;
+  for (int64_t k = 0; k < ne; ++k) {
+    auto key = std::make_pair(c->ei[e0 + k], c->ej[e0 + k]);
+    if (!seen.insert(key).second) {
+      snprintf(buf, sizeof buf, "duplicate edge (%d,%d)", key.first, key.second);
+      v.push_back(buf);
+    }
+  }
+  std::string s;
+  for (size_t i = 0; i < v.size(); ++i) s += (i ? "; " : "") + v[i];
+  return s;
+}
+
+int mgk_upload(mgk_ctx* c, int32_t N, const int64_t* node_off, const int64_t* edge_off, const int32_t* ei,
+               const int32_t* ej, const double* w, const double* p, const double* q, int nl_kind, int nl_dim,
+               const void* node_labels, int el_kind, int el_dim, const void* edge_labels) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (N <= 0) return fail(MGK_E_INVALID, "dataset must hold at least one graph");
+  if (!node_off || !edge_off || !p || !q) return fail(MGK_E_INVALID, "null dataset array");
+  if (nl_kind < 0 || nl_kind > 2 || el_kind < 0 || el_kind > 2) return fail(MGK_E_INVALID, "bad label kind");
+  if (nl_kind == LK_CAT) nl_dim = 1;
+  if (el_kind == LK_CAT) el_dim = 1;
+  if (nl_kind == LK_NONE) nl_dim = 0;
+  if (el_kind == LK_NONE) el_dim = 0;
+  if ((nl_kind && (!node_labels || nl_dim < 1)) || (el_kind && (!edge_labels || el_dim < 1)))
+    return fail(MGK_E_INVALID, "labels declared but missing");
+  c->G = N;
+  c->node_off.assign(node_off, node_off + N + 1);
+  c->edge_off.assign(edge_off, edge_off + N + 1);
+  int64_t nn = c->node_off[N], ne = c->edge_off[N];
+  if (c->node_off[0] != 0 || c->edge_off[0] != 0) return fail(MGK_E_INVALID, "offsets must start at 0");
+  for (int g = 0; g < N; ++g)
+    if (c->node_off[g + 1] < c->node_off[g] || c->edge_off[g + 1] < c->edge_off[g])
+      return fail(MGK_E_INVALID, "offsets must be non-decreasing");
+  if (ne > 0 && (!ei || !ej || !w)) return fail(MGK_E_INVALID, "null edge arrays");
+  c->ei.assign(ei, ei + ne);
+  c->ej.assign(ej, ej + ne);
+  c->w.assign(w, w + ne);
+  c->p.assign(p, p + nn);
+  c->q.assign(q, q + nn);
+  c->nl_kind = nl_kind;
+  c->nl_dim = nl_dim;
+  c->el_kind = el_kind;
+  c->el_dim = el_dim;
+  c->nl_cat.clear();
+  c->nl_vec.clear();
+  c->el_cat.clear();
+  c->el_vec.clear();
+  if (nl_kind == LK_CAT) c->nl_cat.assign((const int64_t*)node_labels, (const int64_t*)node_labels + nn);
+  if (nl_kind == LK_VEC) c->nl_vec.assign((const double*)node_labels, (const double*)node_labels + nn * nl_dim);
+  if (el_kind == LK_CAT) c->el_cat.assign((const int64_t*)edge_labels, (const int64_t*)edge_labels + ne);
+  if (el_kind == LK_VEC) c->el_vec.assign((const double*)edge_labels, (const double*)edge_labels + ne * el_dim);
+  for (int g = 0; g < N; ++g) {
+    if (c->node_off[g + 1] - c->node_off[g] > 65535 * 8)
+      return fail(MGK_E_UNSUPPORTED, "graph %d has more than %d nodes", g, 65535 * 8);
+    std::string v = validate_one(c, g);
+    if (!v.empty()) {
+      c->uploaded = false;
+      return fail(MGK_E_INVALID, "graph %d invalid: %s", g, v.c_str());
+    }
+  }
+  c->uploaded = true;
+  c->prepared = false;
+  return MGK_OK;
+}
+
+int mgk_set_kernels(mgk_ctx* c, const char* vertex_spec, const char* edge_spec) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  Spec vs, es;
+  int rc = parse_spec(vertex_spec, vs);
+  if (rc) return rc;
+  rc = parse_spec(edge_spec, es);
+  if (rc) return rc;
+  c->vspec = vs;
+  c->espec = es;
+  c->prepared = false;
+  return MGK_OK;
+}
+
+// Octiles + degrees for the current (possibly relabelled) dataset.
+static int build_octiles(mgk_ctx* c) {
+  cudaStream_t s = c->stream;
+  const int G = c->G;
+  int64_t ne = c->edge_off[G], nn = c->node_off[G];
+  std::vector<int64_t> gseg(G + 1, 0);
+  std::vector<int32_t> seg_graph, seg_row;
+  for (int g = 0; g < G; ++g) {
+    int n = (int)(c->node_off[g + 1] - c->node_off[g]);
+    int rows = ceil8(n);
+    gseg[g + 1] = gseg[g] + rows;
+    for (int r = 0; r < rows; ++r) {
+      seg_graph.push_back(g);
+      seg_row.push_back(r);
+    }
+  }
+  int64_t nseg = gseg[G];
+  CUDA_TRY(c->d_gseg.upload(gseg, s));
+  CUDA_TRY(c->d_seggraph.upload(seg_graph, s));
+  CUDA_TRY(c->d_segrow.upload(seg_row, s));
+  CUDA_TRY(c->d_ei.upload(c->ei, s));
+  CUDA_TRY(c->d_ej.upload(c->ej, s));
+  CUDA_TRY(c->d_segcount.alloc(nseg));
+  CUDA_TRY(c->d_segcursor.alloc(nseg));
+  CUDA_TRY(c->d_segntiles.alloc(nseg));
+  CUDA_TRY(c->d_segstart.alloc(nseg + 1));
+  CUDA_TRY(c->d_segtile.alloc(nseg + 1));
+  CUDA_TRY(cudaMemsetAsync(c->d_segcount.ptr, 0, nseg * sizeof(int32_t), s));
+  CUDA_TRY(cudaMemsetAsync(c->d_segcursor.ptr, 0, nseg * sizeof(int32_t), s));
+  const int64_t nnz = 2 * ne;
+  CUDA_TRY(c->d_keys.alloc(nnz));
+  CUDA_TRY(c->d_keys2.alloc(2 * nnz));
+  CUDA_TRY(c->d_nzw.alloc(nnz));
+  CUDA_TRY(c->d_nzlabel.alloc(nnz * std::max(c->ds.el_dim, 1)));
+  if (nnz > 0) {
+    int tpb = 256;
+    unsigned grid = (unsigned)((nnz + tpb - 1) / tpb);
+    k_seg_count<<<grid, tpb, 0, s>>>(ne, c->d_ei.ptr, c->d_ej.ptr, c->d_egraph.ptr, c->d_gseg.ptr, c->d_segcount.ptr);
+  }
+  k_scan_exclusive<<<1, 1024, 0, s>>>(nseg, c->d_segcount.ptr, c->d_segstart.ptr);
+  if (nnz > 0) {
+    int tpb = 256;
+    unsigned grid = (unsigned)((nnz + tpb - 1) / tpb);
+    k_seg_scatter<<<grid, tpb, 0, s>>>(ne, c->d_ei.ptr, c->d_ej.ptr, c->d_egraph.ptr, c->d_gseg.ptr,
+                                       c->d_segstart.ptr, c->d_segcursor.ptr, c->d_keys.ptr);
+    CUDA_TRY(cudaFuncSetAttribute(k_seg_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, kSortSmemBytes));
+    unsigned sg = (unsigned)std::min<int64_t>(nseg, (int64_t)c->num_sms * 3);
+    k_seg_sort<<<sg, 256, kSortSmemBytes, s>>>(nseg, c->d_segstart.ptr, c->d_segcount.ptr, c->d_keys.ptr,
+                                               c->d_keys2.ptr);
+  }
+  {
+    unsigned wg = (unsigned)std::min<int64_t>((nseg + 7) / 8, 65535);
+    k_seg_ntiles<<<std::max(wg, 1u), 256, 0, s>>>(nseg, c->d_segstart.ptr, c->d_segcount.ptr, c->d_keys.ptr,
+                                                  c->d_segntiles.ptr);
+  }
+  k_scan_exclusive<<<1, 1024, 0, s>>>(nseg, c->d_segntiles.ptr, c->d_segtile.ptr);
+  int64_t total_tiles = 0;
+  CUDA_TRY(cudaMemcpyAsync(&total_tiles, c->d_segtile.ptr + nseg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  c->total_tiles = total_tiles;
+  CUDA_TRY(c->d_tiles.alloc(total_tiles));
+  CUDA_TRY(cudaMemsetAsync(c->d_tiles.ptr, 0, std::max<int64_t>(total_tiles, 1) * sizeof(Octile), s));
+  if (nnz > 0) {
+    unsigned wg = (unsigned)std::min<int64_t>((nseg + 7) / 8, 65535);
+    k_seg_emit<<<std::max(wg, 1u), 256, 0, s>>>(nseg, c->d_segstart.ptr, c->d_segcount.ptr, c->d_segtile.ptr,
+                                               c->d_seggraph.ptr, c->d_segrow.ptr, c->d_keys.ptr, c->d_graphs.ptr,
+                                               c->d_ew.ptr, c->d_elabel.ptr, c->ds.el_dim, c->d_tiles.ptr,
+                                               c->d_nzw.ptr, c->d_nzlabel.ptr);
+  }
+  k_trow<<<(G + 127) / 128, 128, 0, s>>>(G, c->d_gseg.ptr, c->d_segtile.ptr, c->d_graphs.ptr, c->d_trow.ptr);
+  CUDA_TRY(c->d_deg.alloc(nn));
+  k_degrees<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(nn, c->d_ngraph.ptr, c->d_graphs.ptr, c->d_tiles.ptr,
+                                                         c->d_trow.ptr, c->d_nzw.ptr, c->d_q64.ptr, c->d_deg.ptr);
+  CUDA_TRY(cudaGetLastError());
+  c->graphs.resize(G);
+  CUDA_TRY(cudaMemcpyAsync(c->graphs.data(), c->d_graphs.ptr, G * sizeof(GraphDesc), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  c->ds.tiles = c->d_tiles.ptr;
+  c->ds.trow = c->d_trow.ptr;
+  c->ds.nz_w = c->d_nzw.ptr;
+  c->ds.nz_label = c->d_nzlabel.ptr;
+  c->ds.deg = c->d_deg.ptr;
+  return MGK_OK;
+}
+
+// Lower labels for the current kernels, upload node/edge arrays, build octiles.
+static int prepare(mgk_ctx* c) {
+  if (!c->uploaded) return fail(MGK_E_STATE, "no dataset uploaded");
+  if (c->prepared) return MGK_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const int G = c->G;
+  int64_t nn = c->node_off[G], ne = c->edge_off[G];
+  Lowered vl, el;
+  int rc = lower_labels(c->nl_kind, c->nl_dim, c->nl_cat, c->nl_vec, nn, c->vspec, vl, "node");
+  if (rc) return rc;
+  rc = lower_labels(c->el_kind, c->el_dim, c->el_cat, c->el_vec, ne, c->espec, el, "edge");
+  if (rc) return rc;
+  std::vector<float> p32(nn), q32(nn), w32(ne);
+  std::vector<int32_t> egraph(ne), ngraph(nn);
+  for (int64_t i = 0; i < nn; ++i) {
+    p32[i] = (float)c->p[i];
+    q32[i] = (float)c->q[i];
+  }
+  for (int64_t i = 0; i < ne; ++i) w32[i] = (float)c->w[i];
+  std::vector<GraphDesc> gd(G);
+  int64_t trow_off = 0;
+  for (int g = 0; g < G; ++g) {
+    GraphDesc d{};
+    d.n = (int32_t)(c->node_off[g + 1] - c->node_off[g]);
+    d.ne = (int32_t)(c->edge_off[g + 1] - c->edge_off[g]);
+    d.node_off = c->node_off[g];
+    d.edge_off = c->edge_off[g];
+    d.nz_off = 2 * c->edge_off[g];
+    d.trow_off = trow_off;
+    trow_off += ceil8(d.n) + 1;
+    gd[g] = d;
+    for (int64_t i = c->node_off[g]; i < c->node_off[g + 1]; ++i) ngraph[i] = g;
+    for (int64_t i = c->edge_off[g]; i < c->edge_off[g + 1]; ++i) egraph[i] = g;
+  }
+  CUDA_TRY(c->d_p.upload(p32, s));
+  CUDA_TRY(c->d_q.upload(q32, s));
+  CUDA_TRY(c->d_q64.upload(c->q, s));
+  CUDA_TRY(c->d_ew.upload(w32, s));
+  CUDA_TRY(c->d_vlabel.upload(vl.data, s));
+  CUDA_TRY(c->d_elabel.upload(el.data, s));
+  CUDA_TRY(c->d_egraph.upload(egraph, s));
+  CUDA_TRY(c->d_ngraph.upload(ngraph, s));
+  CUDA_TRY(c->d_graphs.upload(gd, s));
+  CUDA_TRY(c->d_trow.alloc(trow_off));
+  DatasetDev& ds = c->ds;
+  ds = DatasetDev{};
+  ds.G = G;
+  ds.nl_kind = vl.kind;
+  ds.nl_dim = vl.dim;
+  ds.el_kind = el.kind;
+  ds.el_dim = el.dim;
+  ds.graphs = c->d_graphs.ptr;
+  ds.p = c->d_p.ptr;
+  ds.q = c->d_q.ptr;
+  ds.vlabel = c->d_vlabel.ptr;
+  c->vk = to_desc(c->vspec);
+  c->ek = to_desc(c->espec);
+  rc = build_octiles(c);
+  if (rc) return rc;
+  c->prepared = true;
+  return MGK_OK;
+}
+
+int mgk_tiles(mgk_ctx* c, int32_t g, int32_t* ntiles, int32_t* nnz, int32_t* rc_out, uint64_t* bitmap_out,
+              float* w_out) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  int rc = prepare(c);
+  if (rc) return rc;
+  if (g < 0 || g >= c->G) return fail(MGK_E_INVALID, "graph index %d out of range", g);
+  const GraphDesc& d = c->graphs[g];
+  if (ntiles) *ntiles = d.ntiles;
+  if (nnz) *nnz = 2 * d.ne;
+  if (!rc_out && !bitmap_out && !w_out) return MGK_OK;
+  std::vector<Octile> t(d.ntiles);
+  if (d.ntiles)
+    CUDA_TRY(cudaMemcpy(t.data(), c->d_tiles.ptr + d.tile_off, d.ntiles * sizeof(Octile), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < d.ntiles; ++k) {
+    if (rc_out) {
+      rc_out[2 * k] = t[k].row;
+      rc_out[2 * k + 1] = t[k].col;
+    }
+    if (bitmap_out) bitmap_out[k] = t[k].bitmap;
+  }
+  if (w_out && d.ne)
+    CUDA_TRY(cudaMemcpy(w_out, c->d_nzw.ptr + d.nz_off, 2 * d.ne * sizeof(float), cudaMemcpyDeviceToHost));
+  return MGK_OK;
+}
+
+int mgk_degrees(mgk_ctx* c, int32_t g, double* d_out) {
+  if (!c || !d_out) return fail(MGK_E_INVALID, "null argument");
+  int rc = prepare(c);
+  if (rc) return rc;
+  if (g < 0 || g >= c->G) return fail(MGK_E_INVALID, "graph index %d out of range", g);
+  const GraphDesc& d = c->graphs[g];
+  CUDA_TRY(cudaMemcpy(d_out, c->d_deg.ptr + d.node_off, d.n * sizeof(double), cudaMemcpyDeviceToHost));
+  return MGK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Solver dispatch
+// ---------------------------------------------------------------------------
+
+static bool small_graph(const mgk_ctx* c, const GraphDesc& d) {
+  return d.n <= SmallClass::NU && 2 * d.ne <= SmallClass::SMAX && c->ds.el_dim <= 1;
+}
+
+static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
+  SolveParams p{};
+  p.tol2 = tol * tol;
+  p.max_iter = max_iter;
+  p.v_min = 1e-12f;
+  // product.py:153-161 with dataset-uniform label presence; kappa = 1 when ek is None/const1
+  p.labeled = (c->el_kind != LK_NONE && c->espec.kind != KK_NONE && c->espec.kind != KK_CONST1) ? 1 : 0;
+  return p;
+}
+
+struct JobSpec {
+  PairJob job;
+  bool warp;          // small class -> warp kernel
+  int64_t max_n, max_m, max_su, max_sl;
+};
+
+// Per-CTA slab (floats) for the block kernel.
+static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl) {
+  int64_t el = c->ds.el_dim > 2 ? c->ds.el_dim : 0;
+  int64_t f = 5 * n * m + 8 + 4 * (su + sl) + el * (su + sl) + (n + m + 2) + 16;
+  return (f + 31) / 32 * 32;
+}
+
+static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_base,
+                    const std::vector<int64_t>& out_offsets, const SolveParams& prm) {
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c->d_queue.alloc(std::max<size_t>(jobs.size(), 1)));
+  CUDA_TRY(cudaMemsetAsync(c->d_queue.ptr, 0, std::max<size_t>(jobs.size(), 1) * sizeof(unsigned long long), s));
+  // scratch for block jobs
+  int64_t slab = 0;
+  for (auto& j : jobs)
+    if (!j.warp && j.job.npairs > 0) slab = std::max(slab, block_slab(c, j.max_n, j.max_m, j.max_su, j.max_sl));
+  int nctas = 2 * c->num_sms;
+  if (slab > 0) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    int64_t budget = (int64_t)(free_b * 0.6) / 4;
+    int64_t fit = budget / slab;
+    if (fit < nctas) nctas = (int)std::max<int64_t>(fit, 1);
+    CUDA_TRY(c->d_scratch.alloc((size_t)slab * nctas));
+  }
+  c->last_launches = 0;
+  CUDA_TRY(cudaEventRecord(c->ev0, s));
+  for (size_t k = 0; k < jobs.size(); ++k) {
+    JobSpec& j = jobs[k];
+    if (j.job.npairs <= 0) continue;
+    SolveOut o = out_base;
+    int64_t off = out_offsets[k];
+    if (o.value) o.value += off;
+    if (o.iters) o.iters += off;
+    if (o.conv) o.conv += off;
+    if (o.residual) o.residual += off;
+    if (o.nodewise_off) o.nodewise_off += off;
+    cudaError_t e;
+    if (j.warp)
+      e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
+    else
+      e = launch_pcg_block(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slab, nctas, s);
+    if (e != cudaSuccess) return fail(MGK_E_CUDA, "solver launch failed: %s", cudaGetErrorString(e));
+    ++c->last_launches;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev1, s));
+  CUDA_TRY(cudaEventSynchronize(c->ev1));
+  CUDA_TRY(cudaGetLastError());
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  c->last_ms = ms;
+  return MGK_OK;
+}
+
+// Gram jobs: TRI(small) [warp], TRI(other) [block], RECT(other x small) [block];
+// lists are cost-descending (gram.py:38-54: cost = S_a * S_b).
+static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
+  std::vector<int32_t> small, other;
+  for (int g = 0; g < c->G; ++g) (small_graph(c, c->graphs[g]) ? small : other).push_back(g);
+  auto by_cost = [c](int32_t a, int32_t b) {
+    int64_t sa = c->graphs[a].ne, sb = c->graphs[b].ne;
+    return sa != sb ? sa > sb : a < b;
+  };
+  std::stable_sort(small.begin(), small.end(), by_cost);
+  std::stable_sort(other.begin(), other.end(), by_cost);
+  std::vector<int32_t> lists;  // small then other
+  lists.insert(lists.end(), small.begin(), small.end());
+  lists.insert(lists.end(), other.begin(), other.end());
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c->d_list_a.upload(lists, s));
+  const int32_t* dsmall = c->d_list_a.ptr;
+  const int32_t* dother = c->d_list_a.ptr + small.size();
+  auto mx = [c](const std::vector<int32_t>& v, bool nodes) {
+    int64_t r = 0;
+    for (int32_t g : v) r = std::max<int64_t>(r, nodes ? c->graphs[g].n : 2 * c->graphs[g].ne);
+    return r;
+  };
+  int64_t ns = (int64_t)small.size(), no = (int64_t)other.size();
+  JobSpec j1{};
+  j1.job = PairJob{PM_TRI, (int32_t)ns, 0, ns * (ns + 1) / 2, 0, 1, dsmall, nullptr};
+  j1.warp = true;
+  JobSpec j2{};
+  j2.job = PairJob{PM_TRI, (int32_t)no, 0, no * (no + 1) / 2, 0, 1, dother, nullptr};
+  j2.warp = false;
+  j2.max_n = j2.max_m = mx(other, true);
+  j2.max_su = j2.max_sl = mx(other, false);
+  JobSpec j3{};
+  j3.job = PairJob{PM_RECT, (int32_t)no, (int32_t)ns, no * ns, 0, 1, dother, dsmall};
+  j3.warp = false;
+  j3.max_n = mx(other, true);
+  j3.max_m = mx(small, true);
+  j3.max_su = mx(other, false);
+  j3.max_sl = mx(small, false);
+  jobs = {j2, j3, j1};  // big pairs first (longest job first across classes)
+  return MGK_OK;
+}
+
+int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
+  int rc = prepare(c);
+  if (rc) return rc;
+  std::vector<JobSpec> jobs;
+  rc = gram_jobs(c, jobs);
+  if (rc) return rc;
+  int64_t G = c->G;
+  CUDA_TRY(c->d_K.alloc(G * G));
+  CUDA_TRY(c->d_Kit.alloc(G * G));
+  CUDA_TRY(c->d_Kconv.alloc(G * G));
+  SolveOut o{};
+  o.K = c->d_K.ptr;
+  o.K_iters = c->d_Kit.ptr;
+  o.K_conv = c->d_Kconv.ptr;
+  o.G = G;
+  std::vector<int64_t> offs(jobs.size(), 0);
+  rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
+  if (rc) return rc;
+  if (K) CUDA_TRY(cudaMemcpy(K, c->d_K.ptr, G * G * sizeof(double), cudaMemcpyDeviceToHost));
+  if (iters) CUDA_TRY(cudaMemcpy(iters, c->d_Kit.ptr, G * G * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (conv) CUDA_TRY(cudaMemcpy(conv, c->d_Kconv.ptr, G * G, cudaMemcpyDeviceToHost));
+  return MGK_OK;
+}
+
+static int64_t shard_len(int64_t total, int rank, int world) {
+  return total > rank ? (total - rank + world - 1) / world : 0;
+}
+
+int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
+                   double* value, int32_t* iters, uint8_t* conv) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (world < 1 || rank < 0 || rank >= world) return fail(MGK_E_INVALID, "bad rank/world");
+  int rc = prepare(c);
+  if (rc) return rc;
+  std::vector<JobSpec> jobs;
+  rc = gram_jobs(c, jobs);
+  if (rc) return rc;
+  std::vector<int64_t> offs;
+  int64_t total = 0;
+  for (auto& j : jobs) {
+    int64_t len = shard_len(j.job.npairs, rank, world);
+    j.job.offset = rank;
+    j.job.stride = world;
+    j.job.npairs = len;
+    offs.push_back(total);
+    total += len;
+  }
+  if (npairs_out) *npairs_out = total;
+  CUDA_TRY(c->d_value.alloc(total));
+  CUDA_TRY(c->d_iters.alloc(total));
+  CUDA_TRY(c->d_conv.alloc(total));
+  SolveOut o{};
+  o.value = c->d_value.ptr;
+  o.iters = c->d_iters.ptr;
+  o.conv = c->d_conv.ptr;
+  rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
+  if (rc) return rc;
+  if (value) CUDA_TRY(cudaMemcpy(value, c->d_value.ptr, total * sizeof(double), cudaMemcpyDeviceToHost));
+  if (iters) CUDA_TRY(cudaMemcpy(iters, c->d_iters.ptr, total * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (conv) CUDA_TRY(cudaMemcpy(conv, c->d_conv.ptr, total, cudaMemcpyDeviceToHost));
+  return MGK_OK;
+}
+
+int mgk_gram_assemble(mgk_ctx* c, int world, const int64_t* shard_lens, const double* values, const int32_t* iters,
+                      const uint8_t* conv, double* K, int32_t* K_iters, uint8_t* K_conv) {
+  if (!c || !shard_lens || !values || !K) return fail(MGK_E_INVALID, "null argument");
+  int rc = prepare(c);
+  if (rc) return rc;
+  std::vector<JobSpec> jobs;
+  rc = gram_jobs(c, jobs);
+  if (rc) return rc;
+  // host copies of the lists to decode pair ids
+  std::vector<int32_t> lists(c->d_list_a.n);
+  CUDA_TRY(cudaMemcpy(lists.data(), c->d_list_a.ptr, lists.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  const int64_t G = c->G;
+  const double nan = std::nan("");
+  int64_t base = 0;
+  for (int r = 0; r < world; ++r) {
+    int64_t local = 0;
+    for (auto& j : jobs) {
+      PairJob pj = j.job;
+      pj.list_a = lists.data() + (j.job.list_a - c->d_list_a.ptr);
+      pj.list_b = j.job.list_b ? lists.data() + (j.job.list_b - c->d_list_a.ptr) : nullptr;
+      pj.offset = r;
+      pj.stride = world;
+      int64_t len = shard_len(j.job.npairs, r, world);
+      for (int64_t qd = 0; qd < len; ++qd) {
+        int32_t a, b;
+        decode_pair(pj, qd, a, b);
+        int64_t idx = base + local + qd;
+        bool ok = conv ? conv[idx] != 0 : true;
+        double v = ok ? values[idx] : nan;
+        K[a * G + b] = K[b * G + a] = v;
+        if (K_iters) K_iters[a * G + b] = K_iters[b * G + a] = iters ? iters[idx] : 0;
+        if (K_conv) K_conv[a * G + b] = K_conv[b * G + a] = ok;
+      }
+      local += len;
+    }
+    if (local != shard_lens[r]) return fail(MGK_E_INVALID, "shard %d length %lld != expected %lld", r,
+                                            (long long)shard_lens[r], (long long)local);
+    base += local;
+  }
+  return MGK_OK;
+}
+
+int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, double tol, int64_t max_iter,
+              double* value, int32_t* iters, double* residual, uint8_t* conv, double* nodewise) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
+  if (npairs <= 0) return MGK_OK;
+  if (!a || !b) return fail(MGK_E_INVALID, "null pair arrays");
+  int rc = prepare(c);
+  if (rc) return rc;
+  for (int64_t k = 0; k < npairs; ++k)
+    if (a[k] < 0 || a[k] >= c->G || b[k] < 0 || b[k] >= c->G)
+      return fail(MGK_E_INVALID, "pair %lld references unknown graph", (long long)k);
+  // split into warp-class and block-class pairs; outputs in job order, remapped below
+  std::vector<int32_t> wa, wb, ba, bb;
+  std::vector<int64_t> widx, bidx;
+  int64_t bn = 0, bm = 0, bsu = 0, bsl = 0;
+  for (int64_t k = 0; k < npairs; ++k) {
+    const GraphDesc &A = c->graphs[a[k]], &B = c->graphs[b[k]];
+    if (small_graph(c, A) && small_graph(c, B)) {
+      wa.push_back(a[k]);
+      wb.push_back(b[k]);
+      widx.push_back(k);
+    } else {
+      ba.push_back(a[k]);
+      bb.push_back(b[k]);
+      bidx.push_back(k);
+      bn = std::max<int64_t>(bn, A.n);
+      bm = std::max<int64_t>(bm, B.n);
+      bsu = std::max<int64_t>(bsu, 2 * A.ne);
+      bsl = std::max<int64_t>(bsl, 2 * B.ne);
+    }
+  }
+  std::vector<int32_t> la(wa), lb(wb);
+  la.insert(la.end(), ba.begin(), ba.end());
+  lb.insert(lb.end(), bb.begin(), bb.end());
+  std::vector<int64_t> order(widx);
+  order.insert(order.end(), bidx.begin(), bidx.end());
+  cudaStream_t s = c->stream;
+  CUDA_TRY(c->d_list_b.upload(la, s));
+  CUDA_TRY(c->d_list_c.upload(lb, s));
+  std::vector<JobSpec> jobs(2);
+  jobs[0].job = PairJob{PM_LIST, 0, 0, (int64_t)wa.size(), 0, 1, c->d_list_b.ptr, c->d_list_c.ptr};
+  jobs[0].warp = true;
+  jobs[1].job = PairJob{PM_LIST, 0, 0, (int64_t)ba.size(), 0, 1, c->d_list_b.ptr + wa.size(),
+                        c->d_list_c.ptr + wa.size()};
+  jobs[1].warp = false;
+  jobs[1].max_n = bn;
+  jobs[1].max_m = bm;
+  jobs[1].max_su = bsu;
+  jobs[1].max_sl = bsl;
+  std::vector<int64_t> offs = {0, (int64_t)wa.size()};
+  CUDA_TRY(c->d_value.alloc(npairs));
+  CUDA_TRY(c->d_iters.alloc(npairs));
+  CUDA_TRY(c->d_conv.alloc(npairs));
+  CUDA_TRY(c->d_resid.alloc(npairs));
+  SolveOut o{};
+  o.value = c->d_value.ptr;
+  o.iters = c->d_iters.ptr;
+  o.conv = c->d_conv.ptr;
+  o.residual = c->d_resid.ptr;
+  std::vector<int64_t> nwoff(npairs + 1, 0);
+  if (nodewise) {
+    for (int64_t k = 0; k < npairs; ++k)
+      nwoff[k + 1] = nwoff[k] + (int64_t)c->graphs[la[k]].n * c->graphs[lb[k]].n;
+    CUDA_TRY(c->d_nwoff.upload(nwoff, s));
+    CUDA_TRY(c->d_nodewise.alloc(nwoff[npairs]));
+    o.nodewise = c->d_nodewise.ptr;
+    o.nodewise_off = c->d_nwoff.ptr;
+  }
+  rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
+  if (rc) return rc;
+  std::vector<double> hv(npairs);
+  std::vector<int32_t> hi(npairs);
+  std::vector<uint8_t> hc(npairs);
+  std::vector<float> hr(npairs);
+  CUDA_TRY(cudaMemcpy(hv.data(), c->d_value.ptr, npairs * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hi.data(), c->d_iters.ptr, npairs * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hc.data(), c->d_conv.ptr, npairs, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hr.data(), c->d_resid.ptr, npairs * sizeof(float), cudaMemcpyDeviceToHost));
+  std::vector<float> hn;
+  if (nodewise) {
+    hn.resize(nwoff[npairs]);
+    CUDA_TRY(cudaMemcpy(hn.data(), c->d_nodewise.ptr, hn.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  }
+  // output offsets of the caller's order
+  std::vector<int64_t> caller_off(npairs + 1, 0);
+  if (nodewise)
+    for (int64_t k = 0; k < npairs; ++k)
+      caller_off[k + 1] = caller_off[k] + (int64_t)c->graphs[a[k]].n * c->graphs[b[k]].n;
+  for (int64_t j = 0; j < npairs; ++j) {
+    int64_t k = order[j];
+    if (value) value[k] = hv[j];
+    if (iters) iters[k] = hi[j];
+    if (conv) conv[k] = hc[j];
+    if (residual) residual[k] = hr[j];
+    if (nodewise)
+      for (int64_t e = 0; e < nwoff[j + 1] - nwoff[j]; ++e) nodewise[caller_off[k] + e] = hn[nwoff[j] + e];
+  }
+  return MGK_OK;
+}
+
+int mgk_kernel(mgk_ctx* c, int32_t a, int32_t b, double tol, int64_t max_iter, double* value, double* nodewise,
+               int32_t* iters, double* residual, uint8_t* conv) {
+  return mgk_pairs(c, 1, &a, &b, tol, max_iter, value, iters, residual, conv, nodewise);
+}
+
+int mgk_last_timing(mgk_ctx* c, double* solve_ms, int32_t* launches) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (solve_ms) *solve_ms = c->last_ms;
+  if (launches) *launches = c->last_launches;
+  return MGK_OK;
+}
+
+int mgk_reorder(mgk_ctx* c, int method, uint64_t seed, int apply, int64_t* perms_out) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (!c->uploaded) return fail(MGK_E_STATE, "no dataset uploaded");
+  if (method == MGK_REORDER_NONE) {
+    if (perms_out)
+      for (int g = 0; g < c->G; ++g)
+        for (int64_t i = c->node_off[g]; i < c->node_off[g + 1]; ++i) perms_out[i] = i - c->node_off[g];
+    return MGK_OK;
+  }
+  if (method != MGK_REORDER_PBR) return fail(MGK_E_INVALID, "unknown reorder method %d", method);
+  int rc = prepare(c);  // octiles of the current order drive the tile-count fallback
+  if (rc) return rc;
+  std::vector<int64_t> fwd;
+  rc = pbr_device(c->G, c->node_off, c->edge_off, c->ei, c->ej, seed, c->d_tiles.ptr, c->graphs, c->device, c->stream,
+                  fwd, g_err);
+  if (rc) return rc;
+  if (perms_out) std::copy(fwd.begin(), fwd.end(), perms_out);
+  if (apply) {
+    // apply_permutation (reorder.py:86-109): edges (min, max) of forward images, node arrays via inverse
+    std::vector<double> p2(c->p.size()), q2(c->q.size()), nlv(c->nl_vec.size());
+    std::vector<int64_t> nlc(c->nl_cat.size());
+    for (int g = 0; g < c->G; ++g) {
+      int64_t n0 = c->node_off[g];
+      for (int64_t i = n0; i < c->node_off[g + 1]; ++i) {
+        int64_t dst = n0 + fwd[i];
+        p2[dst] = c->p[i];
+        q2[dst] = c->q[i];
+        if (!c->nl_cat.empty()) nlc[dst] = c->nl_cat[i];
+        for (int d = 0; d < c->nl_dim && !c->nl_vec.empty(); ++d) nlv[dst * c->nl_dim + d] = c->nl_vec[i * c->nl_dim + d];
+      }
+      for (int64_t e = c->edge_off[g]; e < c->edge_off[g + 1]; ++e) {
+        int32_t x = (int32_t)fwd[n0 + c->ei[e]], y = (int32_t)fwd[n0 + c->ej[e]];
+        c->ei[e] = std::min(x, y);
+        c->ej[e] = std::max(x, y);
+      }
+    }
+    c->p.swap(p2);
+    c->q.swap(q2);
+    if (!c->nl_cat.empty()) c->nl_cat.swap(nlc);
+    if (!c->nl_vec.empty()) c->nl_vec.swap(nlv);
+    c->prepared = false;
+  }
+  return MGK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+// Device-side data layout shared by the octile builder, the PBR reorder and
+// the PCG solvers.  See DESIGN.md "Data layout in HBM".
+//
+// A dataset of G graphs lives in HBM as structure-of-arrays:
+//   node arrays   [sum n]            p, q (f32), degree (f64 + f32), vertex label
+//   edge arrays   [sum |E|]          i, j (i32), w (f32), edge label (f32 x ED)
+//   octiles       [sum T]            Octile{row, col, nz_off, bitmap}
+//   compact nz    [sum 2|E|]         w (f32), edge label (f32 x ED) in (tile, bit) order
+//   tile-row ptr  [sum (ceil(n/8)+1)] first octile of every tile row (CSR over tile rows)
+// Per-graph offsets (GraphDesc) index into these arrays.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mgk {
+
+constexpr int kTile = 8;
+
+// One non-empty 8x8 block (tiles.py:23-48): bit (r%8)*8 + c%8 set per nonzero;
+// the block's values sit at nz_off .. nz_off+popc(bitmap) in ascending bit order.
+struct __align__(16) Octile {
+  uint16_t row;      // tile row    (r / 8)
+  uint16_t col;      // tile column (c / 8)
+  uint32_t nz_off;   // offset of the first compact value, relative to the graph's nz base
+  uint64_t bitmap;   // occupancy, bit = local_row * 8 + local_col
+};
+
+struct GraphDesc {
+  int32_t n;          // node count
+  int32_t ne;         // undirected edge count (S = 2 ne directed nonzeros)
+  int64_t node_off;   // into node arrays
+  int64_t edge_off;   // into edge arrays
+  int64_t nz_off;     // into compact nz arrays (= 2 * edge_off)
+  int64_t tile_off;   // into octiles
+  int64_t trow_off;   // into tile-row pointer array (ceil(n/8) + 1 entries)
+  int32_t ntiles;     // non-empty octiles
+  int32_t pad;
+};
+
+// Base-kernel descriptor (basekernels.py:60-172); kind codes match basekernels.py.
+enum KernelKind : int32_t { KK_CONST1 = 0, KK_DELTA = 1, KK_SE = 2, KK_POLY = 3, KK_NONE = 4 };
+constexpr int kMaxPoly = 8;
+struct KernelDesc {
+  int32_t kind;
+  int32_t ncoef;
+  float h;             // delta baseline
+  float alpha;         // SE alpha
+  float se_scale;      // sqrt(alpha * log2(e)): labels are pre-scaled so SE = exp2(-|a-b|^2)
+  float coef[kMaxPoly];
+};
+
+// Label storage kinds (graphs.py:126-146).
+enum LabelKind : int32_t { LK_NONE = 0, LK_CAT = 1, LK_VEC = 2 };
+
+constexpr int kMaxLabelDim = 4;
+
+struct DatasetDev {
+  int32_t G;
+  int32_t nl_kind, nl_dim;     // vertex labels
+  int32_t el_kind, el_dim;     // edge labels
+  const GraphDesc* graphs;
+  // node arrays
+  const float* p;
+  const float* q;
+  const double* deg;           // d_i = sum_j w_ij + q_i, accumulated in ascending column order (f64)
+  const float* vlabel;         // [sum n * nl_dim]  (categorical tokens stored as int bits)
+  // octiles
+  const Octile* tiles;
+  const int32_t* trow;         // tile-row pointers, relative to the graph's tile_off
+  const float* nz_w;           // [sum S]
+  const float* nz_label;       // [sum S * el_dim]
+};
+
+__host__ __device__ inline int ceil8(int n) { return (n + 7) >> 3; }
+
+// kappa(a, b) for scalar labels with the descriptor semantics.
+// SE labels are pre-scaled by se_scale, so kappa = exp2(-(a-b)^2).
+__device__ __forceinline__ float kernel_scalar(const KernelDesc& k, float a, float b) {
+  switch (k.kind) {
+    case KK_DELTA:
+      return (a == b) ? 1.0f : k.h;
+    case KK_SE: {
+      float d = a - b;
+      return exp2f(-d * d);
+    }
+    case KK_POLY: {
+      float d = fabsf(a - b);
+      float acc = 0.0f;
+      for (int c = k.ncoef - 1; c >= 0; --c) acc = fmaf(acc, d, k.coef[c]);
+      return fminf(fmaxf(acc, 0.0f), 1.0f);
+    }
+    default:
+      return 1.0f;
+  }
+}
+
+// Vector-label version (dim <= kMaxLabelDim); categorical labels compare as ints.
+__device__ __forceinline__ float kernel_vec(const KernelDesc& k, const float* a, const float* b, int dim,
+                                            bool categorical) {
+  switch (k.kind) {
+    case KK_DELTA: {
+      bool eq = true;
+      if (categorical) {
+        for (int c = 0; c < dim; ++c) eq &= (__float_as_int(a[c]) == __float_as_int(b[c]));
+      } else {
+        for (int c = 0; c < dim; ++c) eq &= (a[c] == b[c]);
+      }
+      return eq ? 1.0f : k.h;
+    }
+    case KK_SE: {
+      float s = 0.0f;
+      for (int c = 0; c < dim; ++c) {
+        float d = a[c] - b[c];
+        s = fmaf(d, d, s);
+      }
+      return exp2f(-s);
+    }
+    case KK_POLY:
+      return kernel_scalar(k, a[0], b[0]);
+    default:
+      return 1.0f;
+  }
+}
+
+}  // namespace mgk

@@ -1,0 +1,102 @@
+// Internal declarations shared by the .cu translation units of libmgk.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mgk_dev.cuh"
+
+namespace mgk {
+
+// How a solver launch enumerates its pairs (all map a pair id to (a, b)).
+enum PairMode : int32_t {
+  PM_TRI = 0,   // all u <= v over list_a (row-major); list sorted by cost descending
+  PM_RECT = 1,  // list_a x list_b
+  PM_LIST = 2,  // explicit pairs: list_a[k], list_b[k]
+};
+
+struct PairJob {
+  int32_t mode;
+  int32_t na, nb;           // list lengths
+  int64_t npairs;           // pairs this launch solves (after sharding)
+  int64_t offset, stride;   // shard: local id q -> global id offset + q * stride
+  const int32_t* list_a;
+  const int32_t* list_b;
+};
+
+struct SolveOut {
+  // Gram matrix outputs (mirrored writes), any may be null
+  double* K;                // [G*G]
+  int32_t* K_iters;         // [G*G]
+  uint8_t* K_conv;          // [G*G]
+  int64_t G;
+  // per-pair outputs (indexed by pair id), any may be null
+  double* value;
+  int32_t* iters;
+  uint8_t* conv;
+  float* residual;
+  // nodewise field x[i * m + i'] per pair (float32), offsets per pair id
+  float* nodewise;
+  const int64_t* nodewise_off;
+};
+
+struct SolveParams {
+  double tol2;              // tol^2 (relative stopping rule r.r < tol^2 b.b)
+  int64_t max_iter;         // 0 -> 10 * n * m (solver.py:87)
+  float v_min;              // vertex-similarity floor (product.py:172-175)
+  int32_t labeled;          // edge mode decided per dataset (product.py:153-161)
+};
+
+__host__ __device__ inline void decode_pair(const PairJob& j, int64_t q, int32_t& a, int32_t& b) {
+  const int64_t pid = j.offset + q * j.stride;
+  if (j.mode == PM_LIST) {
+    a = j.list_a[pid];
+    b = j.list_b[pid];
+  } else if (j.mode == PM_RECT) {
+    a = j.list_a[pid / j.nb];
+    b = j.list_b[pid % j.nb];
+  } else {
+    // row u holds (u, u..n-1); start(u) = u*n - u*(u-1)/2
+    int64_t n = j.na;
+    double disc = (double)(2 * n + 1) * (double)(2 * n + 1) - 8.0 * (double)pid;
+    int64_t u = (int64_t)(((double)(2 * n + 1) - sqrt(disc > 0 ? disc : 0.0)) * 0.5);
+    if (u < 0) u = 0;
+    if (u > n - 1) u = n - 1;
+    auto start = [n](int64_t r) { return r * n - r * (r - 1) / 2; };
+    while (u > 0 && start(u) > pid) --u;
+    while (u + 1 < n && start(u + 1) <= pid) ++u;
+    int64_t v = pid - start(u) + u;
+    a = j.list_a[u];
+    b = j.list_a[v];
+  }
+}
+
+// ---- tile builder kernels (tiles.cu)
+__global__ void k_seg_count(int64_t, const int32_t*, const int32_t*, const int32_t*, const int64_t*, int32_t*);
+__global__ void k_seg_scatter(int64_t, const int32_t*, const int32_t*, const int32_t*, const int64_t*,
+                              const int64_t*, int32_t*, uint64_t*);
+__global__ void k_seg_sort(int64_t, const int64_t*, const int32_t*, uint64_t*, uint64_t*);
+__global__ void k_seg_ntiles(int64_t, const int64_t*, const int32_t*, const uint64_t*, int32_t*);
+__global__ void k_seg_emit(int64_t, const int64_t*, const int32_t*, const int64_t*, const int32_t*,
+                           const int32_t*, const uint64_t*, const GraphDesc*, const float*, const float*, int,
+                           Octile*, float*, float*);
+__global__ void k_degrees(int64_t, const int32_t*, const GraphDesc*, const Octile*, const int32_t*,
+                          const float*, const double*, double*);
+__global__ void k_scan_exclusive(int64_t, const int32_t*, int64_t*);
+__global__ void k_trow(int, const int64_t*, const int64_t*, GraphDesc*, int32_t*);
+constexpr int kSortSmemBytes = 8192 * 8;
+
+// ---- solvers (pcg_warp.cu, pcg_block.cu)
+struct SmallClass {
+  static constexpr int NU = 24;      // max nodes of either graph
+  static constexpr int SLOTS = 10;   // lane-side nonzeros <= 32 * SLOTS
+  static constexpr int SMAX = 32 * SLOTS;
+};
+
+cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                            const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
+                            int num_sms, cudaStream_t stream);
+cudaError_t launch_pcg_block(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
+                             float* scratch, int64_t scratch_floats_per_cta, int nctas, cudaStream_t stream);
+
+}  // namespace mgk

@@ -1,0 +1,247 @@
+"""ctypes binding of libmgk.so (the C-ABI in include/mgk.h).
+
+The product path has no CPU fallback: if the shared object is missing, or no
+CUDA device is visible, every compute call raises ``NativeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("MGK_LIB", HERE / "libmgk.so"))
+
+MGK_E_INVALID, MGK_E_SHAPE, MGK_E_CUDA, MGK_E_UNSUPPORTED, MGK_E_STATE = -1, -2, -3, -4, -5
+LABEL_NONE, LABEL_CAT, LABEL_VEC = 0, 1, 2
+
+# name -> (restype, argtypes); the authoritative list of exported symbols
+_P = C.c_void_p
+SIGNATURES = {
+    "mgk_version": (C.c_char_p, []),
+    "mgk_last_error": (C.c_char_p, []),
+    "mgk_ctx_create": (C.c_int, [C.POINTER(_P), C.c_int]),
+    "mgk_ctx_destroy": (C.c_int, [_P]),
+    "mgk_upload": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, C.c_int, C.c_int, _P, C.c_int, C.c_int, _P]),
+    "mgk_set_kernels": (C.c_int, [_P, C.c_char_p, C.c_char_p]),
+    "mgk_reorder": (C.c_int, [_P, C.c_int, C.c_uint64, C.c_int, _P]),
+    "mgk_tiles": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P]),
+    "mgk_degrees": (C.c_int, [_P, C.c_int32, _P]),
+    "mgk_gram": (C.c_int, [_P, C.c_double, C.c_int64, _P, _P, _P]),
+    "mgk_gram_shard": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, _P, _P, _P, _P]),
+    "mgk_gram_assemble": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
+    "mgk_pairs": (C.c_int, [_P, C.c_int64, _P, _P, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
+    "mgk_kernel": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
+    "mgk_last_timing": (C.c_int, [_P, _P, _P]),
+}
+
+
+class NativeError(RuntimeError):
+    """libmgk failed (missing library, no device, CUDA error)."""
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: Path | None = None):
+    """Load libmgk.so and bind every symbol of SIGNATURES (fails loudly)."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path or LIB_PATH)
+        if not p.exists():
+            raise NativeError(f"libmgk.so not found at {p}; build it with `python -m paper_1910_06310_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = C.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def check(rc: int):
+    if rc == 0:
+        return
+    msg = load().mgk_last_error().decode(errors="replace")
+    from .basekernels import KernelShapeError
+
+    if rc == MGK_E_INVALID:
+        raise ValueError(msg)
+    if rc == MGK_E_SHAPE:
+        raise KernelShapeError(msg)
+    if rc == MGK_E_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise NativeError(msg)
+
+
+class Context:
+    """Owns one mgk_ctx (one CUDA device)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load()
+        h = C.c_void_p()
+        check(self.lib.mgk_ctx_create(C.byref(h), int(device)))
+        self.h = h
+        self.G = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.mgk_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, packed: "PackedDataset"):
+        pk = packed
+        check(self.lib.mgk_upload(
+            self.h, pk.G, _ptr(pk.node_off), _ptr(pk.edge_off), _ptr(pk.ei), _ptr(pk.ej), _ptr(pk.w), _ptr(pk.p),
+            _ptr(pk.q), pk.nl_kind, pk.nl_dim, _ptr(pk.node_labels), pk.el_kind, pk.el_dim, _ptr(pk.edge_labels)))
+        self.G = pk.G
+        self.packed = pk
+
+    def set_kernels(self, vspec: str | None, espec: str | None):
+        check(self.lib.mgk_set_kernels(self.h, (vspec or "").encode(), (espec or "").encode()))
+
+    def reorder_pbr(self, seed: int, apply: bool) -> np.ndarray:
+        out = np.empty(int(self.packed.node_off[-1]), dtype=np.int64)
+        check(self.lib.mgk_reorder(self.h, 1, C.c_uint64(seed & ((1 << 64) - 1)), int(apply), _ptr(out)))
+        return out
+
+    def tiles(self, g: int):
+        nt, nz = C.c_int32(), C.c_int32()
+        check(self.lib.mgk_tiles(self.h, int(g), C.byref(nt), C.byref(nz), None, None, None))
+        rc = np.empty(2 * nt.value, dtype=np.int32)
+        bm = np.empty(nt.value, dtype=np.uint64)
+        w = np.empty(nz.value, dtype=np.float32)
+        check(self.lib.mgk_tiles(self.h, int(g), C.byref(nt), C.byref(nz), _ptr(rc), _ptr(bm), _ptr(w)))
+        return rc.reshape(-1, 2), bm, w
+
+    def degrees(self, g: int, n: int) -> np.ndarray:
+        d = np.empty(n, dtype=np.float64)
+        check(self.lib.mgk_degrees(self.h, int(g), _ptr(d)))
+        return d
+
+    def gram(self, tol: float, max_iter: int = 0, fetch: bool = True):
+        G = self.G
+        if not fetch:
+            check(self.lib.mgk_gram(self.h, float(tol), int(max_iter), None, None, None))
+            return None
+        K = np.empty((G, G), dtype=np.float64)
+        it = np.empty((G, G), dtype=np.int32)
+        cv = np.empty((G, G), dtype=np.uint8)
+        check(self.lib.mgk_gram(self.h, float(tol), int(max_iter), _ptr(K), _ptr(it), _ptr(cv)))
+        return K, it, cv.astype(bool)
+
+    def gram_shard(self, rank: int, world: int, tol: float, max_iter: int = 0):
+        n = C.c_int64()
+        check(self.lib.mgk_gram_shard(self.h, rank, world, float(tol), int(max_iter), C.byref(n), None, None, None))
+        v = np.empty(n.value, dtype=np.float64)
+        it = np.empty(n.value, dtype=np.int32)
+        cv = np.empty(n.value, dtype=np.uint8)
+        check(self.lib.mgk_gram_shard(self.h, rank, world, float(tol), int(max_iter), C.byref(n), _ptr(v), _ptr(it),
+                                      _ptr(cv)))
+        return v, it, cv
+
+    def gram_assemble(self, world: int, lens, values, iters, conv):
+        G = self.G
+        lens = np.ascontiguousarray(lens, dtype=np.int64)
+        K = np.empty((G, G), dtype=np.float64)
+        Ki = np.empty((G, G), dtype=np.int32)
+        Kc = np.empty((G, G), dtype=np.uint8)
+        check(self.lib.mgk_gram_assemble(self.h, world, _ptr(lens), _ptr(np.ascontiguousarray(values, np.float64)),
+                                         _ptr(np.ascontiguousarray(iters, np.int32)),
+                                         _ptr(np.ascontiguousarray(conv, np.uint8)), _ptr(K), _ptr(Ki), _ptr(Kc)))
+        return K, Ki, Kc.astype(bool)
+
+    def pairs(self, a, b, tol: float, max_iter: int = 0, nodewise: bool = False, sizes=None):
+        a = np.ascontiguousarray(a, dtype=np.int32)
+        b = np.ascontiguousarray(b, dtype=np.int32)
+        k = len(a)
+        val = np.empty(k, dtype=np.float64)
+        it = np.empty(k, dtype=np.int32)
+        res = np.empty(k, dtype=np.float64)
+        cv = np.empty(k, dtype=np.uint8)
+        nw = None
+        if nodewise:
+            n = np.asarray(sizes, dtype=np.int64)
+            nw = np.empty(int(np.sum(n[a] * n[b])), dtype=np.float64)
+        check(self.lib.mgk_pairs(self.h, k, _ptr(a), _ptr(b), float(tol), int(max_iter), _ptr(val), _ptr(it),
+                                 _ptr(res), _ptr(cv), _ptr(nw)))
+        return val, it, res, cv.astype(bool), nw
+
+    def last_timing(self):
+        ms, n = C.c_double(), C.c_int32()
+        check(self.lib.mgk_last_timing(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+
+class PackedDataset:
+    """Graphs packed into the flat arrays mgk_upload takes (the device layout's host image)."""
+
+    def __init__(self, graphs, with_labels: bool = True):
+        from .basekernels import KernelShapeError
+
+        graphs = list(graphs)
+        if not graphs:
+            raise ValueError("dataset must hold at least one graph")
+        self.G = len(graphs)
+        n = np.array([g.node_count for g in graphs], dtype=np.int64)
+        e = np.array([len(g.weights) for g in graphs], dtype=np.int64)
+        self.sizes = n
+        self.nnz = 2 * e
+        self.node_off = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+        self.edge_off = np.concatenate([[0], np.cumsum(e)]).astype(np.int64)
+        cat = lambda xs, dt: np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros(0), dtype=dt)  # noqa: E731
+        self.ei = cat([np.asarray(g.edges_i) for g in graphs], np.int32)
+        self.ej = cat([np.asarray(g.edges_j) for g in graphs], np.int32)
+        self.w = cat([np.asarray(g.weights, float) for g in graphs], np.float64)
+        self.p = cat([np.asarray(g.start_prob, float) for g in graphs], np.float64)
+        self.q = cat([np.asarray(g.stop_prob, float) for g in graphs], np.float64)
+        self.nl_kind, self.nl_dim, self.node_labels = LABEL_NONE, 0, None
+        self.el_kind, self.el_dim, self.edge_labels = LABEL_NONE, 0, None
+        if with_labels:
+            self.nl_kind, self.nl_dim, self.node_labels = self._labels([g.node_labels for g in graphs], "node", n,
+                                                                       KernelShapeError, None)
+            self.el_kind, self.el_dim, self.edge_labels = self._labels([g.edge_labels for g in graphs], "edge", e,
+                                                                       KernelShapeError, e)
+
+    @staticmethod
+    def _labels(labs, what, counts, err, edge_counts):
+        # presence must be uniform (product.py:158-159, 170-171); edgeless graphs carry no evidence
+        present = [lab is not None for lab in labs]
+        relevant = [p for p, c in zip(present, counts) if (edge_counts is None or c > 0)]
+        if not any(present):
+            return LABEL_NONE, 0, None
+        if any(relevant) and not all(relevant):
+            raise err(f"{what} label presence must be uniform across a pair")
+        kinds = {("c" if np.asarray(lab).dtype.kind in "iu" else "v") for lab in labs if lab is not None}
+        if len(kinds) > 1:
+            raise err(f"{what} label kinds differ across the dataset")
+        if kinds == {"c"}:
+            data = [np.asarray(lab, np.int64).reshape(-1) if lab is not None else np.zeros(c, np.int64)
+                    for lab, c in zip(labs, counts)]
+            return LABEL_CAT, 1, np.ascontiguousarray(np.concatenate(data), dtype=np.int64)
+        dims = {np.asarray(lab).reshape(len(lab), -1).shape[1] for lab in labs if lab is not None and len(lab)}
+        if len(dims) > 1:
+            raise err(f"label dimensions differ: {sorted(dims)}")
+        d = dims.pop() if dims else 1
+        data = [np.asarray(lab, np.float64).reshape(-1, d) if lab is not None else np.zeros((c, d))
+                for lab, c in zip(labs, counts)]
+        return LABEL_VEC, d, np.ascontiguousarray(np.concatenate(data).reshape(-1), dtype=np.float64)

