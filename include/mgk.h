@@ -86,18 +86,15 @@ int mgk_degrees(mgk_ctx* ctx, int32_t g, double* d_out);
  * device-resident benchmark).  max_iter 0 -> 10*n*m (solver.py:87). */
 int mgk_gram(mgk_ctx* ctx, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv);
 
-/* Shard of the Gram pairs for multi-GPU runs: this context solves the pairs
- * whose cost-ordered id is congruent to rank modulo world, writing compact
- * per-pair results in that order (value, iterations, converged).  *npairs_out
- * receives the shard length. */
+/* Shard of the Gram pairs for multi-GPU runs (the per-GPU part of the
+ * 8-GPU pair scheduling in north_star; the reference's equivalent is the
+ * pair queue of gram.py:69-86): this context solves the pairs whose
+ * cost-ordered id is congruent to rank modulo world and writes compact
+ * per-pair results (graph ids a, b, value, iterations, converged).  Call
+ * with all outputs NULL to learn *npairs_out; the results of the last call
+ * also stay on the device. */
 int mgk_gram_shard(mgk_ctx* ctx, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
-                   double* value, int32_t* iters, uint8_t* conv);
-
-/* Scatter gathered shard results into the Gram matrix (mirrored, NaN where
- * not converged).  values/iters/conv hold world shards concatenated in rank
- * order with the lengths mgk_gram_shard reported. */
-int mgk_gram_assemble(mgk_ctx* ctx, int world, const int64_t* shard_len, const double* values, const int32_t* iters,
-                      const uint8_t* conv, double* K, int32_t* K_iters, uint8_t* K_conv);
+                   int32_t* pair_a, int32_t* pair_b, double* value, int32_t* iters, uint8_t* conv);
 
 /* Batch of explicit pairs (the per-pair `kernel` of solver.py:212-246 without
  * reordering): value[k], iters[k], residual[k], conv[k]; nodewise (nullable)
@@ -112,6 +109,15 @@ int mgk_kernel(mgk_ctx* ctx, int32_t a, int32_t b, double tol, int64_t max_iter,
 /* Device time (ms, CUDA events on the solver stream) and the number of
  * kernel launches of the last solve call. */
 int mgk_last_timing(mgk_ctx* ctx, double* solve_ms, int32_t* launches);
+
+/* Benchmark support (not part of the reference interface): measured FP32
+ * FFMA throughput (TFLOP/s) and MUFU ex2 throughput (T ops/s) of `device`,
+ * the denominators of the roofline fractions bench.py reports. */
+int mgk_bench_peaks(int device, double* fp32_tflops, double* ex2_tops);
+
+/* Benchmark support: cumulative host->device and device->host payload bytes
+ * moved by this process's libmgk calls (for end-to-end accounting). */
+int mgk_transfer_bytes(int64_t* h2d, int64_t* d2h);
 
 #ifdef __cplusplus
 }

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -20,6 +21,13 @@ using namespace mgk;
 namespace {
 
 thread_local std::string g_err;
+// cumulative host<->device payload bytes (benchmark accounting)
+int64_t g_h2d_bytes = 0, g_d2h_bytes = 0;
+
+cudaError_t d2h(void* dst, const void* src, size_t bytes) {
+  g_d2h_bytes += (int64_t)bytes;
+  return cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+}
 
 int fail(int code, const char* fmt, ...) {
   char buf[4096];
@@ -60,6 +68,7 @@ struct DBuf {
   cudaError_t upload(const std::vector<T>& v, cudaStream_t s) {
     cudaError_t e = alloc(v.size());
     if (e != cudaSuccess || v.empty()) return e;
+    g_h2d_bytes += (int64_t)(v.size() * sizeof(T));
     return cudaMemcpyAsync(ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
   }
 };
@@ -209,6 +218,8 @@ struct mgk_ctx {
   DBuf<uint8_t> d_Kconv, d_conv;
   DBuf<float> d_resid, d_scratch, d_nodewise;
   DBuf<int64_t> d_nwoff;
+  DBuf<int32_t> d_pa, d_pb, d_rowcol;
+  DBuf<int64_t> d_rowpre;
 };
 
 extern "C" {
@@ -524,7 +535,7 @@ int mgk_tiles(mgk_ctx* c, int32_t g, int32_t* ntiles, int32_t* nnz, int32_t* rc_
   if (!rc_out && !bitmap_out && !w_out) return MGK_OK;
   std::vector<Octile> t(d.ntiles);
   if (d.ntiles)
-    CUDA_TRY(cudaMemcpy(t.data(), c->d_tiles.ptr + d.tile_off, d.ntiles * sizeof(Octile), cudaMemcpyDeviceToHost));
+    CUDA_TRY(d2h(t.data(), c->d_tiles.ptr + d.tile_off, d.ntiles * sizeof(Octile)));
   for (int k = 0; k < d.ntiles; ++k) {
     if (rc_out) {
       rc_out[2 * k] = t[k].row;
@@ -533,7 +544,7 @@ int mgk_tiles(mgk_ctx* c, int32_t g, int32_t* ntiles, int32_t* nnz, int32_t* rc_
     if (bitmap_out) bitmap_out[k] = t[k].bitmap;
   }
   if (w_out && d.ne)
-    CUDA_TRY(cudaMemcpy(w_out, c->d_nzw.ptr + d.nz_off, 2 * d.ne * sizeof(float), cudaMemcpyDeviceToHost));
+    CUDA_TRY(d2h(w_out, c->d_nzw.ptr + d.nz_off, 2 * d.ne * sizeof(float)));
   return MGK_OK;
 }
 
@@ -543,7 +554,7 @@ int mgk_degrees(mgk_ctx* c, int32_t g, double* d_out) {
   if (rc) return rc;
   if (g < 0 || g >= c->G) return fail(MGK_E_INVALID, "graph index %d out of range", g);
   const GraphDesc& d = c->graphs[g];
-  CUDA_TRY(cudaMemcpy(d_out, c->d_deg.ptr + d.node_off, d.n * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(d2h(d_out, c->d_deg.ptr + d.node_off, d.n * sizeof(double)));
   return MGK_OK;
 }
 
@@ -555,21 +566,31 @@ static bool small_graph(const mgk_ctx* c, const GraphDesc& d) {
   return d.n <= SmallClass::NU && 2 * d.ne <= SmallClass::SMAX && c->ds.el_dim <= 1;
 }
 
+// n * m at or below which a small pair is solved by the FP64 tiny kernel
+static int tiny_nm() {
+  const char* t = getenv("MGK_TINY_NM");
+  return t ? atoi(t) : 128;
+}
+
 static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   SolveParams p{};
   p.tol2 = tol * tol;
   p.max_iter = max_iter;
   p.v_min = 1e-12f;
+  p.tiny_nm = tiny_nm();
   // product.py:153-161 with dataset-uniform label presence; kappa = 1 when ek is None/const1
   p.labeled = (c->el_kind != LK_NONE && c->espec.kind != KK_NONE && c->espec.kind != KK_CONST1) ? 1 : 0;
   return p;
 }
 
+enum JobKernel { JK_BLOCK = 0, JK_WARP = 1, JK_TINY = 2 };
+
 struct JobSpec {
   PairJob job;
-  bool warp;          // small class -> warp kernel
+  int kernel;         // JobKernel
   int64_t max_n, max_m, max_su, max_sl;
 };
+
 
 // Per-CTA slab (floats) for the block kernel.
 static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl) {
@@ -586,7 +607,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   // scratch for block jobs
   int64_t slab = 0;
   for (auto& j : jobs)
-    if (!j.warp && j.job.npairs > 0) slab = std::max(slab, block_slab(c, j.max_n, j.max_m, j.max_su, j.max_sl));
+    if (j.kernel == JK_BLOCK && j.job.npairs > 0) slab = std::max(slab, block_slab(c, j.max_n, j.max_m, j.max_su, j.max_sl));
   int nctas = 2 * c->num_sms;
   if (slab > 0) {
     size_t free_b = 0, total_b = 0;
@@ -608,9 +629,13 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     if (o.conv) o.conv += off;
     if (o.residual) o.residual += off;
     if (o.nodewise_off) o.nodewise_off += off;
+    if (o.pair_a) o.pair_a += off;
+    if (o.pair_b) o.pair_b += off;
     cudaError_t e;
-    if (j.warp)
+    if (j.kernel == JK_WARP)
       e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
+    else if (j.kernel == JK_TINY)
+      e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
     else
       e = launch_pcg_block(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slab, nctas, s);
     if (e != cudaSuccess) return fail(MGK_E_CUDA, "solver launch failed: %s", cudaGetErrorString(e));
@@ -625,46 +650,77 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   return MGK_OK;
 }
 
-// Gram jobs: TRI(small) [warp], TRI(other) [block], RECT(other x small) [block];
-// lists are cost-descending (gram.py:38-54: cost = S_a * S_b).
+// Gram jobs (all pairs a <= b, gram.py:57-95), cost-descending within each:
+//   small graphs sorted by (n, S) descending; the pairs of row u are split at
+//   c(u) = first column whose n_u * n_v <= tiny_nm into a main ragged job
+//   [warp kernel, FP32] and a tiny ragged job [tiny kernel, FP64];
+//   pairs with a larger graph: TRI(other) + RECT(other x small) [block kernel].
 static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   std::vector<int32_t> small, other;
   for (int g = 0; g < c->G; ++g) (small_graph(c, c->graphs[g]) ? small : other).push_back(g);
-  auto by_cost = [c](int32_t a, int32_t b) {
-    int64_t sa = c->graphs[a].ne, sb = c->graphs[b].ne;
-    return sa != sb ? sa > sb : a < b;
+  auto by_size = [c](int32_t a, int32_t b) {
+    const GraphDesc &x = c->graphs[a], &y = c->graphs[b];
+    if (x.n != y.n) return x.n > y.n;
+    if (x.ne != y.ne) return x.ne > y.ne;
+    return a < b;
   };
-  std::stable_sort(small.begin(), small.end(), by_cost);
-  std::stable_sort(other.begin(), other.end(), by_cost);
+  std::stable_sort(small.begin(), small.end(), by_size);
+  std::stable_sort(other.begin(), other.end(), by_size);
+  const int64_t ns = (int64_t)small.size(), no = (int64_t)other.size();
+  const int T = tiny_nm();
+  // ragged rows over the size-sorted small list
+  std::vector<int64_t> mpre(ns + 1, 0), tpre(ns + 1, 0);
+  std::vector<int32_t> mcol(ns), tcol(ns);
+  int64_t cu = ns;  // c(u) is non-decreasing in u (n descending)
+  int64_t v = 0;
+  for (int64_t u = 0; u < ns; ++u) {
+    const int64_t nu = c->graphs[small[u]].n;
+    while (v < ns && (int64_t)c->graphs[small[v]].n * nu > T) ++v;
+    cu = v;
+    const int64_t split = std::max<int64_t>(u, cu);
+    mcol[u] = (int32_t)u;
+    mpre[u + 1] = mpre[u] + (split - u);
+    tcol[u] = (int32_t)split;
+    tpre[u + 1] = tpre[u] + (ns - split);
+  }
+  cudaStream_t s = c->stream;
   std::vector<int32_t> lists;  // small then other
   lists.insert(lists.end(), small.begin(), small.end());
   lists.insert(lists.end(), other.begin(), other.end());
-  cudaStream_t s = c->stream;
   CUDA_TRY(c->d_list_a.upload(lists, s));
+  std::vector<int64_t> pre(mpre);
+  pre.insert(pre.end(), tpre.begin(), tpre.end());
+  std::vector<int32_t> col(mcol);
+  col.insert(col.end(), tcol.begin(), tcol.end());
+  CUDA_TRY(c->d_rowpre.upload(pre, s));
+  CUDA_TRY(c->d_rowcol.upload(col, s));
   const int32_t* dsmall = c->d_list_a.ptr;
   const int32_t* dother = c->d_list_a.ptr + small.size();
-  auto mx = [c](const std::vector<int32_t>& v, bool nodes) {
+  auto mx = [c](const std::vector<int32_t>& vv, bool nodes) {
     int64_t r = 0;
-    for (int32_t g : v) r = std::max<int64_t>(r, nodes ? c->graphs[g].n : 2 * c->graphs[g].ne);
+    for (int32_t g : vv) r = std::max<int64_t>(r, nodes ? c->graphs[g].n : 2 * c->graphs[g].ne);
     return r;
   };
-  int64_t ns = (int64_t)small.size(), no = (int64_t)other.size();
-  JobSpec j1{};
-  j1.job = PairJob{PM_TRI, (int32_t)ns, 0, ns * (ns + 1) / 2, 0, 1, dsmall, nullptr};
-  j1.warp = true;
+  JobSpec jm{};
+  jm.job = PairJob{PM_RAGGED, (int32_t)ns, 0, mpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr, c->d_rowcol.ptr};
+  jm.kernel = JK_WARP;
+  JobSpec jt{};
+  jt.job = PairJob{PM_RAGGED, (int32_t)ns, 0, tpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr + ns + 1,
+                   c->d_rowcol.ptr + ns};
+  jt.kernel = JK_TINY;
   JobSpec j2{};
-  j2.job = PairJob{PM_TRI, (int32_t)no, 0, no * (no + 1) / 2, 0, 1, dother, nullptr};
-  j2.warp = false;
+  j2.job = PairJob{PM_TRI, (int32_t)no, 0, no * (no + 1) / 2, 0, 1, dother, nullptr, nullptr, nullptr};
+  j2.kernel = JK_BLOCK;
   j2.max_n = j2.max_m = mx(other, true);
   j2.max_su = j2.max_sl = mx(other, false);
   JobSpec j3{};
-  j3.job = PairJob{PM_RECT, (int32_t)no, (int32_t)ns, no * ns, 0, 1, dother, dsmall};
-  j3.warp = false;
+  j3.job = PairJob{PM_RECT, (int32_t)no, (int32_t)ns, no * ns, 0, 1, dother, dsmall, nullptr, nullptr};
+  j3.kernel = JK_BLOCK;
   j3.max_n = mx(other, true);
   j3.max_m = mx(small, true);
   j3.max_su = mx(other, false);
   j3.max_sl = mx(small, false);
-  jobs = {j2, j3, j1};  // big pairs first (longest job first across classes)
+  jobs = {j2, j3, jm, jt};  // big pairs first (longest job first across classes)
   return MGK_OK;
 }
 
@@ -688,9 +744,9 @@ int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters
   std::vector<int64_t> offs(jobs.size(), 0);
   rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
   if (rc) return rc;
-  if (K) CUDA_TRY(cudaMemcpy(K, c->d_K.ptr, G * G * sizeof(double), cudaMemcpyDeviceToHost));
-  if (iters) CUDA_TRY(cudaMemcpy(iters, c->d_Kit.ptr, G * G * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (conv) CUDA_TRY(cudaMemcpy(conv, c->d_Kconv.ptr, G * G, cudaMemcpyDeviceToHost));
+  if (K) CUDA_TRY(d2h(K, c->d_K.ptr, G * G * sizeof(double)));
+  if (iters) CUDA_TRY(d2h(iters, c->d_Kit.ptr, G * G * sizeof(int32_t)));
+  if (conv) CUDA_TRY(d2h(conv, c->d_Kconv.ptr, G * G));
   return MGK_OK;
 }
 
@@ -699,9 +755,10 @@ static int64_t shard_len(int64_t total, int rank, int world) {
 }
 
 int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
-                   double* value, int32_t* iters, uint8_t* conv) {
+                   int32_t* pair_a, int32_t* pair_b, double* value, int32_t* iters, uint8_t* conv) {
   if (!c) return fail(MGK_E_INVALID, "null context");
   if (world < 1 || rank < 0 || rank >= world) return fail(MGK_E_INVALID, "bad rank/world");
+  if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
   int rc = prepare(c);
   if (rc) return rc;
   std::vector<JobSpec> jobs;
@@ -718,60 +775,25 @@ int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter
     total += len;
   }
   if (npairs_out) *npairs_out = total;
+  if (!pair_a && !pair_b && !value && !iters && !conv) return MGK_OK;
   CUDA_TRY(c->d_value.alloc(total));
   CUDA_TRY(c->d_iters.alloc(total));
   CUDA_TRY(c->d_conv.alloc(total));
+  CUDA_TRY(c->d_pa.alloc(total));
+  CUDA_TRY(c->d_pb.alloc(total));
   SolveOut o{};
   o.value = c->d_value.ptr;
   o.iters = c->d_iters.ptr;
   o.conv = c->d_conv.ptr;
+  o.pair_a = c->d_pa.ptr;
+  o.pair_b = c->d_pb.ptr;
   rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
   if (rc) return rc;
-  if (value) CUDA_TRY(cudaMemcpy(value, c->d_value.ptr, total * sizeof(double), cudaMemcpyDeviceToHost));
-  if (iters) CUDA_TRY(cudaMemcpy(iters, c->d_iters.ptr, total * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (conv) CUDA_TRY(cudaMemcpy(conv, c->d_conv.ptr, total, cudaMemcpyDeviceToHost));
-  return MGK_OK;
-}
-
-int mgk_gram_assemble(mgk_ctx* c, int world, const int64_t* shard_lens, const double* values, const int32_t* iters,
-                      const uint8_t* conv, double* K, int32_t* K_iters, uint8_t* K_conv) {
-  if (!c || !shard_lens || !values || !K) return fail(MGK_E_INVALID, "null argument");
-  int rc = prepare(c);
-  if (rc) return rc;
-  std::vector<JobSpec> jobs;
-  rc = gram_jobs(c, jobs);
-  if (rc) return rc;
-  // host copies of the lists to decode pair ids
-  std::vector<int32_t> lists(c->d_list_a.n);
-  CUDA_TRY(cudaMemcpy(lists.data(), c->d_list_a.ptr, lists.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  const int64_t G = c->G;
-  const double nan = std::nan("");
-  int64_t base = 0;
-  for (int r = 0; r < world; ++r) {
-    int64_t local = 0;
-    for (auto& j : jobs) {
-      PairJob pj = j.job;
-      pj.list_a = lists.data() + (j.job.list_a - c->d_list_a.ptr);
-      pj.list_b = j.job.list_b ? lists.data() + (j.job.list_b - c->d_list_a.ptr) : nullptr;
-      pj.offset = r;
-      pj.stride = world;
-      int64_t len = shard_len(j.job.npairs, r, world);
-      for (int64_t qd = 0; qd < len; ++qd) {
-        int32_t a, b;
-        decode_pair(pj, qd, a, b);
-        int64_t idx = base + local + qd;
-        bool ok = conv ? conv[idx] != 0 : true;
-        double v = ok ? values[idx] : nan;
-        K[a * G + b] = K[b * G + a] = v;
-        if (K_iters) K_iters[a * G + b] = K_iters[b * G + a] = iters ? iters[idx] : 0;
-        if (K_conv) K_conv[a * G + b] = K_conv[b * G + a] = ok;
-      }
-      local += len;
-    }
-    if (local != shard_lens[r]) return fail(MGK_E_INVALID, "shard %d length %lld != expected %lld", r,
-                                            (long long)shard_lens[r], (long long)local);
-    base += local;
-  }
+  if (pair_a) CUDA_TRY(d2h(pair_a, c->d_pa.ptr, total * sizeof(int32_t)));
+  if (pair_b) CUDA_TRY(d2h(pair_b, c->d_pb.ptr, total * sizeof(int32_t)));
+  if (value) CUDA_TRY(d2h(value, c->d_value.ptr, total * sizeof(double)));
+  if (iters) CUDA_TRY(d2h(iters, c->d_iters.ptr, total * sizeof(int32_t)));
+  if (conv) CUDA_TRY(d2h(conv, c->d_conv.ptr, total));
   return MGK_OK;
 }
 
@@ -786,16 +808,18 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
   for (int64_t k = 0; k < npairs; ++k)
     if (a[k] < 0 || a[k] >= c->G || b[k] < 0 || b[k] >= c->G)
       return fail(MGK_E_INVALID, "pair %lld references unknown graph", (long long)k);
-  // split into warp-class and block-class pairs; outputs in job order, remapped below
-  std::vector<int32_t> wa, wb, ba, bb;
-  std::vector<int64_t> widx, bidx;
+  // split into tiny / warp-class / block-class pairs; outputs in job order, remapped below
+  std::vector<int32_t> ta, tb, wa, wb, ba, bb;
+  std::vector<int64_t> tidx, widx, bidx;
   int64_t bn = 0, bm = 0, bsu = 0, bsl = 0;
+  const int T = tiny_nm();
   for (int64_t k = 0; k < npairs; ++k) {
     const GraphDesc &A = c->graphs[a[k]], &B = c->graphs[b[k]];
     if (small_graph(c, A) && small_graph(c, B)) {
-      wa.push_back(a[k]);
-      wb.push_back(b[k]);
-      widx.push_back(k);
+      const bool tiny = (int64_t)A.n * B.n <= T;
+      (tiny ? ta : wa).push_back(a[k]);
+      (tiny ? tb : wb).push_back(b[k]);
+      (tiny ? tidx : widx).push_back(k);
     } else {
       ba.push_back(a[k]);
       bb.push_back(b[k]);
@@ -807,24 +831,30 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
     }
   }
   std::vector<int32_t> la(wa), lb(wb);
+  la.insert(la.end(), ta.begin(), ta.end());
+  lb.insert(lb.end(), tb.begin(), tb.end());
   la.insert(la.end(), ba.begin(), ba.end());
   lb.insert(lb.end(), bb.begin(), bb.end());
   std::vector<int64_t> order(widx);
+  order.insert(order.end(), tidx.begin(), tidx.end());
   order.insert(order.end(), bidx.begin(), bidx.end());
   cudaStream_t s = c->stream;
   CUDA_TRY(c->d_list_b.upload(la, s));
   CUDA_TRY(c->d_list_c.upload(lb, s));
-  std::vector<JobSpec> jobs(2);
-  jobs[0].job = PairJob{PM_LIST, 0, 0, (int64_t)wa.size(), 0, 1, c->d_list_b.ptr, c->d_list_c.ptr};
-  jobs[0].warp = true;
-  jobs[1].job = PairJob{PM_LIST, 0, 0, (int64_t)ba.size(), 0, 1, c->d_list_b.ptr + wa.size(),
-                        c->d_list_c.ptr + wa.size()};
-  jobs[1].warp = false;
-  jobs[1].max_n = bn;
-  jobs[1].max_m = bm;
-  jobs[1].max_su = bsu;
-  jobs[1].max_sl = bsl;
-  std::vector<int64_t> offs = {0, (int64_t)wa.size()};
+  const int64_t nw0 = (int64_t)wa.size(), nt0 = (int64_t)ta.size();
+  std::vector<JobSpec> jobs(3);
+  jobs[0].job = PairJob{PM_LIST, 0, 0, nw0, 0, 1, c->d_list_b.ptr, c->d_list_c.ptr, nullptr, nullptr};
+  jobs[0].kernel = JK_WARP;
+  jobs[1].job = PairJob{PM_LIST, 0, 0, nt0, 0, 1, c->d_list_b.ptr + nw0, c->d_list_c.ptr + nw0, nullptr, nullptr};
+  jobs[1].kernel = JK_TINY;
+  jobs[2].job = PairJob{PM_LIST, 0, 0, (int64_t)ba.size(), 0, 1, c->d_list_b.ptr + nw0 + nt0,
+                        c->d_list_c.ptr + nw0 + nt0, nullptr, nullptr};
+  jobs[2].kernel = JK_BLOCK;
+  jobs[2].max_n = bn;
+  jobs[2].max_m = bm;
+  jobs[2].max_su = bsu;
+  jobs[2].max_sl = bsl;
+  std::vector<int64_t> offs = {0, nw0, nw0 + nt0};
   CUDA_TRY(c->d_value.alloc(npairs));
   CUDA_TRY(c->d_iters.alloc(npairs));
   CUDA_TRY(c->d_conv.alloc(npairs));
@@ -849,14 +879,14 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
   std::vector<int32_t> hi(npairs);
   std::vector<uint8_t> hc(npairs);
   std::vector<float> hr(npairs);
-  CUDA_TRY(cudaMemcpy(hv.data(), c->d_value.ptr, npairs * sizeof(double), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(hi.data(), c->d_iters.ptr, npairs * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(hc.data(), c->d_conv.ptr, npairs, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(hr.data(), c->d_resid.ptr, npairs * sizeof(float), cudaMemcpyDeviceToHost));
+  CUDA_TRY(d2h(hv.data(), c->d_value.ptr, npairs * sizeof(double)));
+  CUDA_TRY(d2h(hi.data(), c->d_iters.ptr, npairs * sizeof(int32_t)));
+  CUDA_TRY(d2h(hc.data(), c->d_conv.ptr, npairs));
+  CUDA_TRY(d2h(hr.data(), c->d_resid.ptr, npairs * sizeof(float)));
   std::vector<float> hn;
   if (nodewise) {
     hn.resize(nwoff[npairs]);
-    CUDA_TRY(cudaMemcpy(hn.data(), c->d_nodewise.ptr, hn.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    CUDA_TRY(d2h(hn.data(), c->d_nodewise.ptr, hn.size() * sizeof(float)));
   }
   // output offsets of the caller's order
   std::vector<int64_t> caller_off(npairs + 1, 0);
@@ -878,6 +908,12 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
 int mgk_kernel(mgk_ctx* c, int32_t a, int32_t b, double tol, int64_t max_iter, double* value, double* nodewise,
                int32_t* iters, double* residual, uint8_t* conv) {
   return mgk_pairs(c, 1, &a, &b, tol, max_iter, value, iters, residual, conv, nodewise);
+}
+
+int mgk_transfer_bytes(int64_t* h2d, int64_t* d2h_out) {
+  if (h2d) *h2d = g_h2d_bytes;
+  if (d2h_out) *d2h_out = g_d2h_bytes;
+  return MGK_OK;
 }
 
 int mgk_last_timing(mgk_ctx* c, double* solve_ms, int32_t* launches) {

@@ -12,6 +12,7 @@ enum PairMode : int32_t {
   PM_TRI = 0,   // all u <= v over list_a (row-major); list sorted by cost descending
   PM_RECT = 1,  // list_a x list_b
   PM_LIST = 2,  // explicit pairs: list_a[k], list_b[k]
+  PM_RAGGED = 3,  // row u of list_a pairs with list_a[col0[u] .. col0[u] + len(u)); rows by prefix
 };
 
 struct PairJob {
@@ -21,6 +22,8 @@ struct PairJob {
   int64_t offset, stride;   // shard: local id q -> global id offset + q * stride
   const int32_t* list_a;
   const int32_t* list_b;
+  const int64_t* row_prefix;  // PM_RAGGED: na + 1 prefix counts of row lengths
+  const int32_t* row_col0;    // PM_RAGGED: first column of each row
 };
 
 struct SolveOut {
@@ -34,6 +37,8 @@ struct SolveOut {
   int32_t* iters;
   uint8_t* conv;
   float* residual;
+  int32_t* pair_a;          // graph ids of each solved pair
+  int32_t* pair_b;
   // nodewise field x[i * m + i'] per pair (float32), offsets per pair id
   float* nodewise;
   const int64_t* nodewise_off;
@@ -44,6 +49,7 @@ struct SolveParams {
   int64_t max_iter;         // 0 -> 10 * n * m (solver.py:87)
   float v_min;              // vertex-similarity floor (product.py:172-175)
   int32_t labeled;          // edge mode decided per dataset (product.py:153-161)
+  int32_t tiny_nm;          // n*m at or below which the warp solver runs the pair in FP64
 };
 
 __host__ __device__ inline void decode_pair(const PairJob& j, int64_t q, int32_t& a, int32_t& b) {
@@ -51,6 +57,14 @@ __host__ __device__ inline void decode_pair(const PairJob& j, int64_t q, int32_t
   if (j.mode == PM_LIST) {
     a = j.list_a[pid];
     b = j.list_b[pid];
+  } else if (j.mode == PM_RAGGED) {
+    int lo = 0, hi = j.na;  // largest u with row_prefix[u] <= pid
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (j.row_prefix[mid] <= pid) lo = mid; else hi = mid;
+    }
+    a = j.list_a[lo];
+    b = j.list_a[j.row_col0[lo] + (pid - j.row_prefix[lo])];
   } else if (j.mode == PM_RECT) {
     a = j.list_a[pid / j.nb];
     b = j.list_b[pid % j.nb];
@@ -93,6 +107,9 @@ struct SmallClass {
 };
 
 cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                            const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
+                            int num_sms, cudaStream_t stream);
+cudaError_t launch_pcg_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                             int num_sms, cudaStream_t stream);
 cudaError_t launch_pcg_block(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,

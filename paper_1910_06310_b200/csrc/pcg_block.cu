@@ -269,6 +269,8 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
       if (out.iters) out.iters[pid] = (int32_t)it;
       if (out.conv) out.conv[pid] = conv ? 1 : 0;
       if (out.residual) out.residual[pid] = (float)sqrt(rr);
+      if (out.pair_a) out.pair_a[pid] = ga;
+      if (out.pair_b) out.pair_b[pid] = gb;
       if (out.K) {
         double kval = conv ? val : __longlong_as_double(0x7ff8000000000000ll);
         out.K[(int64_t)ga * out.G + gb] = kval;

@@ -12,24 +12,25 @@
 //
 // Roles.  Of the two graphs, U ("uniform") is walked row by row by the whole
 // warp in lock step, L ("lanes") is spread over the 32 lanes: lane l owns the
-// L-nonzeros k' = l + 32 t (t < SLOTS, held in registers for the whole solve)
-// and the L-node i' = l for the vector operations.  The PCG vectors live in
+// L-nonzeros k' = l + 32 t (t < NS, registers, for the whole solve) and the
+// L-node i' = l for the vector operations.  The PCG direction P lives in
 // shared memory as [i][32] (i = U node, column = lane), so the XMV gather
-// P[j][col_L(k')] is bank-conflict free (bank = column) and every vector op is
-// lane-local.  For U-row i:
+// P[j][col_L(k')] is bank-conflict free (bank = column).  For U-row i:
 //
 //   acc[t] = sum_{k in U(i)} kappa(e_k, e'_t) * w_k * P[j_k][col_L(t)]   (registers)
-//   SEG[k'] = acc[t] * w'_t;  AP[i][i'] = diag * P[i][i'] - sum_{k' in L(i')} SEG[k']
+//   SEG[k'] = acc[t] * w'_t;  OFF[i][i'] = sum_{k' in L(i')} SEG[k']
 //
-// i.e. exactly sum_{j, j'} w_ij w'_i'j' ke(e_ij, e'_i'j') p[j, j'] (product.py:454-478).
-// Unlabeled pairs use the factorised form AP = D.P - A (P B^T) (the paper's
-// dense x dense unlabeled primitive, product.py:94), which costs
-// n*S_L + S_U*m instead of S_U*S_L.
+// i.e. OFF = sum_{j, j'} w_ij w'_i'j' ke(e_ij, e'_i'j') p[j, j'] (product.py:454-478),
+// and the vector phase forms A p = diag * p - OFF.  NS = ceil(S_L / 32) is a
+// template parameter (switch per pair) so no lane issues dead slots.
+// Unlabeled pairs use the factorised form OFF = A (P B^T) (the paper's dense x
+// dense unlabeled primitive, product.py:94): n*S_L + S_U*m work instead of
+// S_U*S_L.  The value px.x is accumulated as sum_k alpha_k (px.p_k), so the
+// Gram path keeps no x vector.
 //
 // The octile format is what the warp reads from HBM: the prologue expands the
 // two graphs' octiles (16-byte records, one 64-bit bitmap each) into per-row
-// neighbour lists with popc/bit-scan, which is also how rows are ordered
-// (ascending column, as the reference's tile order implies).
+// nonzero lists with popc/bit-scan (ascending column, as the tile order implies).
 #include <cstdio>
 
 #include "mgk_internal.h"
@@ -37,23 +38,36 @@
 namespace mgk {
 
 constexpr int kWarpsPerBlock = 2;
+constexpr int NU = SmallClass::NU;
+constexpr int SLOTS = SmallClass::SLOTS;
+constexpr int SMAX = SmallClass::SMAX;
 
-template <int NU, int SLOTS, bool UNLAB>
+template <bool UNLAB, bool NODEWISE>
 struct WarpSmem {
-  float P[NU][32];
-  float AP[NU][32];      // + DG: staging area for the L nonzeros during the prologue
-  float DG[NU][32];
+  float P[NU][32];        // P + OFF: staging area for the L nonzeros during the prologue
+  float OFF[NU][32];
+  float R[NU][32];        // residual
+  float DG[NU][32];       // diagonal d_i d'_l / kv
   float T[UNLAB ? NU : 1][32];
-  float4 UE[32 * SLOTS]; // U nonzeros in row order: {col (int bits), w, label, 0}
-  float SEG[32 * SLOTS];
+  float X[NODEWISE ? NU : 1][32];
+  float2 UWL[SMAX];       // U nonzeros in row order: {w, label}
+  int UOFF[SMAX];         //   and the byte offset of P row j (j * 128)
+  float SEG[2 * 32 * SLOTS];  // segment sums of two U-rows
   int urow[NU + 8];
-  float upq[NU];         // p_i (start probability) of U nodes
-  float udq[NU];         // d_i q_i of U nodes
+  int lrow[40];
+  float upq[NU];          // p_i of U nodes
+  float udq[NU];          // d_i q_i of U nodes
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -89,36 +103,35 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
   return v;
 }
 
-// Expand a graph's octiles into row-ordered nonzeros {col, w, label} at dst and
-// row pointers at rowptr[0..n] (lane i handles row i; n <= 32).
-__device__ void octiles_to_rows(const DatasetDev& ds, const GraphDesc& g, int lane, float4* dst, int* rowptr,
-                                int el_dim) {
+// Expand a graph's octiles into row-ordered nonzeros (lane i handles row i;
+// n <= 32); emit(pos, col, w, label) receives them, rowptr[0..n] the offsets.
+template <typename Emit>
+__device__ __forceinline__ void octiles_to_rows(const DatasetDev& ds, const GraphDesc& g, int lane, int* rowptr,
+                                                int el_dim, Emit emit) {
   int cnt = 0;
   const int32_t* tr = ds.trow + g.trow_off;
   const Octile* tiles = ds.tiles + g.tile_off;
-  int I = lane >> 3, r = lane & 7;
+  const int I = lane >> 3, r = lane & 7;
   int t0 = 0, t1 = 0;
   if (lane < g.n) {
     t0 = tr[I];
     t1 = tr[I + 1];
     for (int t = t0; t < t1; ++t) cnt += __popc((uint32_t)(tiles[t].bitmap >> (8 * r)) & 0xffu);
   }
-  int incl = warp_incl_scan(cnt, lane);
-  int start = incl - cnt;
-  if (lane < g.n) rowptr[lane] = start;
+  const int incl = warp_incl_scan(cnt, lane);
+  int pos = incl - cnt;
+  if (lane < g.n) rowptr[lane] = pos;
   if (lane == g.n - 1) rowptr[g.n] = incl;
   if (lane < g.n) {
     const float* w = ds.nz_w + g.nz_off;
     const float* lab = ds.nz_label + g.nz_off * el_dim;
     for (int t = t0; t < t1; ++t) {
-      Octile o = tiles[t];
+      const Octile o = tiles[t];
       uint32_t byte = (uint32_t)(o.bitmap >> (8 * r)) & 0xffu;
-      int base = o.nz_off + __popcll(o.bitmap & ((1ull << (8 * r)) - 1ull));
+      const int base = o.nz_off + __popcll(o.bitmap & ((1ull << (8 * r)) - 1ull));
       for (int c = 0; byte; ++c, byte &= byte - 1) {
-        int lc = __ffs(byte) - 1;
-        int k = base + c;
-        float l0 = el_dim > 0 ? lab[(int64_t)k * el_dim] : 0.0f;
-        dst[start++] = make_float4(__int_as_float(o.col * 8 + lc), w[k], l0, 0.0f);
+        const int k = base + c;
+        emit(pos++, o.col * 8 + (__ffs(byte) - 1), w[k], el_dim > 0 ? lab[(int64_t)k * el_dim] : 0.0f);
       }
     }
   }
@@ -131,6 +144,8 @@ __device__ __forceinline__ void write_pair_outputs(const SolveOut& out, unsigned
   if (out.iters) out.iters[pid] = (int32_t)it;
   if (out.conv) out.conv[pid] = conv ? 1 : 0;
   if (out.residual) out.residual[pid] = (float)sqrt(rr);
+  if (out.pair_a) out.pair_a[pid] = ga;
+  if (out.pair_b) out.pair_b[pid] = gb;
   const double kval = conv ? val : __longlong_as_double(0x7ff8000000000000ll);
   if (out.K) {
     out.K[(int64_t)ga * out.G + gb] = kval;
@@ -146,19 +161,32 @@ __device__ __forceinline__ void write_pair_outputs(const SolveOut& out, unsigned
   }
 }
 
-// Tiny product systems (n*m <= kTinyNM, or self pairs whose symmetric subspace
-// is that small): CG terminates there by Krylov exhaustion, which FP32
-// rounding in the matvec delays by a few iterations.  These pairs run the
-// same algorithm with FP64 vectors and FP64 accumulation (coefficients stay
-// FP32), which restores the reference's iteration counts; element e of the
-// field is owned by lane e % 32.
-constexpr int kTinyNM = 128;
+// diag[i][l] = d_i d'_l / max(kv, v_min)  (product.py:164-178, 210); kept out of
+// line so the vertex-kernel code exists once per kernel (instruction-cache footprint)
+__device__ __noinline__ double diag_of(const DatasetDev& ds, const KernelDesc& vk, const SolveParams& prm,
+                                          bool vlab, int64_t vu, int64_t vl) {
+  float kv = 1.0f;
+  if (vlab)
+    kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
+                          ds.nl_kind == LK_CAT), prm.v_min);
+  return ds.deg[vu] * ds.deg[vl] / (double)kv;
+}
+
+// ---------------------------------------------------------------------------
+// Tiny product systems (n*m <= prm.tiny_nm, default 128): CG terminates there
+// by Krylov exhaustion, which FP32 rounding in the matvec delays by a few
+// iterations.  These pairs run the same algorithm with FP64 vectors and FP64
+// accumulation (coefficients stay FP32), which restores the reference's
+// iteration counts; element e of the field is owned by lane e % 32.
+// ---------------------------------------------------------------------------
+constexpr int kTinyMax = 128;
 
 template <int EK>
-__device__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
-                           const GraphDesc& U, const GraphDesc& L, const float4* ue, const int* urow,
-                           const float4* le, const int* lrow, double* P, double* AP, double* DG, int lane,
-                           double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw, bool swap) {
+__device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
+                           const GraphDesc& U, const GraphDesc& L, const float2* uwl, const int* uoff,
+                           const int* urow, const float4* le, const int* lrow, double* P, double* AP, double* DG,
+                           int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw,
+                           bool swap) {
   const int nu = U.n, m = L.n, nm = nu * m;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
   double r[4], x[4];
@@ -174,21 +202,17 @@ __device__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const Ker
   double rho = 0.0, rr = 0.0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    int e = lane + 32 * s;
+    const int e = lane + 32 * s;
     r[s] = 0.0;
     x[s] = 0.0;
     if (e < nm) {
-      int i = e / m, l = e - i * m;
-      int64_t vu = U.node_off + i, vl = L.node_off + l;
-      float kv = 1.0f;
-      if (vlab)
-        kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
-                              ds.nl_kind == LK_CAT), prm.v_min);
-      double dg = ds.deg[vu] * ds.deg[vl] / (double)kv;
-      double b = (ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]);
+      const int i = e / m, l = e - i * m;
+      const int64_t vu = U.node_off + i, vl = L.node_off + l;
+      const double dg = diag_of(ds, vk, prm, vlab, vu, vl);
+      const double b = (ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]);
       DG[e] = dg;
       r[s] = b;
-      double z = b / dg;
+      const double z = b / dg;
       P[e] = z;
       rho += b * z;
       rr += b * b;
@@ -204,16 +228,16 @@ __device__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const Ker
   while (!conv && it < max_iter) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      int e = lane + 32 * s;
+      const int e = lane + 32 * s;
       if (e < nm) {
-        int i = e / m, l = e - i * m;
+        const int i = e / m, l = e - i * m;
         double acc = 0.0;
         for (int k = urow[i]; k < urow[i + 1]; ++k) {
-          const float4 a = ue[k];
-          const double* prow = P + __float_as_int(a.x) * m;
+          const float2 a = uwl[k];
+          const double* prow = P + (uoff[k] >> 7) * m;
           for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
             const float4 b = le[q];
-            float c = edge_kappa<EK>(ek, a.z, b.z) * a.y * b.y;
+            const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
             acc = fma((double)c, prow[__float_as_int(b.x)], acc);
           }
         }
@@ -225,14 +249,14 @@ __device__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const Ker
     double pap = 0.0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      int e = lane + 32 * s;
+      const int e = lane + 32 * s;
       if (e < nm) pap += P[e] * AP[e];
     }
     const double alpha = rho / warp_sum(pap);
     double rr_l = 0.0, rz_l = 0.0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      int e = lane + 32 * s;
+      const int e = lane + 32 * s;
       if (e < nm) {
         x[s] += alpha * P[e];
         r[s] -= alpha * AP[e];
@@ -250,7 +274,7 @@ __device__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const Ker
     __syncwarp();
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-      int e = lane + 32 * s;
+      const int e = lane + 32 * s;
       if (e < nm) P[e] = r[s] / DG[e] + beta * P[e];
     }
     rho = rho_next;
@@ -259,9 +283,9 @@ __device__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const Ker
   double val = 0.0;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    int e = lane + 32 * s;
+    const int e = lane + 32 * s;
     if (e < nm) {
-      int i = e / m, l = e - i * m;
+      const int i = e / m, l = e - i * m;
       val += (double)ds.p[U.node_off + i] * (double)ds.p[L.node_off + l] * x[s];
       if (nw) nw[swap ? (int64_t)l * nu + i : (int64_t)e] = (float)x[s];
     }
@@ -272,19 +296,145 @@ __device__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const Ker
   rr_out = rr;
 }
 
-template <int NU, int SLOTS, int EK>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+// ---------------------------------------------------------------------------
+// XMV, labeled: OFF[i][l] for all U-rows i, NS slots per lane.
+// ---------------------------------------------------------------------------
+// acc[t] += sum_{k in U(i)} kappa(e_k, e'_t) w_k P[j_k][col_L(t)]  (row i of U)
+template <int NS, int EK, class Smem>
+__device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& ek, int i, const char* pbase,
+                                               const int (&lcoff)[SLOTS], const float (&llab)[SLOTS],
+                                               float (&acc)[NS]) {
+  const int k1 = S.urow[i + 1];
+  int k = S.urow[i];
+  for (; k + 1 < k1; k += 2) {
+    const float2 e0 = S.UWL[k], e1 = S.UWL[k + 1];
+    const char* r0 = pbase + S.UOFF[k];
+    const char* r1 = pbase + S.UOFF[k + 1];
+    float p0[NS], p1[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      p0[t] = *reinterpret_cast<const float*>(r0 + lcoff[t]);
+      p1[t] = *reinterpret_cast<const float*>(r1 + lcoff[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      acc[t] = fmaf(edge_kappa<EK>(ek, e0.y, llab[t]), e0.x * p0[t], acc[t]);
+      acc[t] = fmaf(edge_kappa<EK>(ek, e1.y, llab[t]), e1.x * p1[t], acc[t]);
+    }
+  }
+  if (k < k1) {
+    const float2 e0 = S.UWL[k];
+    const char* r0 = pbase + S.UOFF[k];
+#pragma unroll
+    for (int t = 0; t < NS; ++t)
+      acc[t] = fmaf(edge_kappa<EK>(ek, e0.y, llab[t]), e0.x * *reinterpret_cast<const float*>(r0 + lcoff[t]),
+                    acc[t]);
+  }
+}
+
+// Two U-rows per pass: one SEG round trip and one pair of warp syncs per two
+// rows, and two independent summation chains in the segment reduction.
+template <int NS, int EK, class Smem>
+__device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int nu, int m, int lane,
+                                            const int (&lcoff)[SLOTS], const float (&lw)[SLOTS],
+                                            const float (&llab)[SLOTS], int lr0, int lr1) {
+  const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
+  for (int i = 0; i < nu; i += 2) {
+    const bool two = i + 1 < nu;
+    float acc0[NS], acc1[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) acc0[t] = acc1[t] = 0.0f;
+    accumulate_row<NS, EK>(S, ek, i, pbase, lcoff, llab, acc0);
+    if (two) accumulate_row<NS, EK>(S, ek, i + 1, pbase, lcoff, llab, acc1);
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      S.SEG[lane + 32 * t] = acc0[t] * lw[t];
+      S.SEG[32 * SLOTS + lane + 32 * t] = acc1[t] * lw[t];
+    }
+    __syncwarp();
+    if (lane < m) {
+      float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 2
+      for (int q = lr0; q < lr1; ++q) {
+        s0 += S.SEG[q];
+        s1 += S.SEG[32 * SLOTS + q];
+      }
+      S.OFF[i][lane] = s0;
+      if (two) S.OFF[i + 1][lane] = s1;
+    }
+    __syncwarp();
+  }
+}
+
+// XMV, unlabeled (kappa = 1): T = P B^T (slots + segment sums), OFF = A T.
+template <int NS, class Smem>
+__device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, const int (&lcoff)[SLOTS],
+                                              const float (&lw)[SLOTS], int lr0, int lr1) {
+  const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
+  for (int j = 0; j < nu; ++j) {
+    const char* row = pbase + j * 128;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) S.SEG[lane + 32 * t] = lw[t] * *reinterpret_cast<const float*>(row + lcoff[t]);
+    __syncwarp();
+    if (lane < m) {
+      float s = 0.0f;
+#pragma unroll 1
+      for (int q = lr0; q < lr1; ++q) s += S.SEG[q];
+      S.T[j][lane] = s;
+    }
+    __syncwarp();
+  }
+  for (int i = 0; i < nu; ++i) {
+    float s = 0.0f;
+    for (int k = S.urow[i]; k < S.urow[i + 1]; ++k) s = fmaf(S.UWL[k].x, S.T[S.UOFF[k] >> 7][lane], s);
+    if (lane < m) S.OFF[i][lane] = s;
+  }
+  __syncwarp();
+}
+
+template <int EK, class Smem>
+__device__ __forceinline__ void xmv_dispatch(int ns, Smem& S, const KernelDesc& ek, int nu, int m, int lane,
+                                             const int (&lcoff)[SLOTS], const float (&lw)[SLOTS],
+                                             const float (&llab)[SLOTS], int lr0, int lr1) {
+#define MGK_XMV_CASE(N)                                                     \
+  case N:                                                                   \
+    if constexpr (EK == KK_NONE)                                            \
+      xmv_unlabeled<N>(S, nu, m, lane, lcoff, lw, lr0, lr1);                \
+    else                                                                    \
+      xmv_labeled<N, EK>(S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);    \
+    break;
+  switch (ns) {
+    MGK_XMV_CASE(1)
+    MGK_XMV_CASE(2)
+    MGK_XMV_CASE(3)
+    MGK_XMV_CASE(4)
+    MGK_XMV_CASE(5)
+    MGK_XMV_CASE(6)
+    MGK_XMV_CASE(7)
+    MGK_XMV_CASE(8)
+    MGK_XMV_CASE(9)
+    MGK_XMV_CASE(10)
+    default:  // ns == 0: edgeless lane graph, OFF = 0
+      for (int i = 0; i < nu; ++i) S.OFF[i][lane] = 0.0f;
+      __syncwarp();
+  }
+#undef MGK_XMV_CASE
+  static_assert(SLOTS == 10, "xmv_dispatch covers 1..10 slots");
+}
+
+template <int EK, bool NODEWISE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 6)
 k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
            unsigned long long* queue) {
   constexpr bool UNLAB = (EK == KK_NONE);
-  using Smem = WarpSmem<NU, SLOTS, UNLAB>;
-  static_assert(sizeof(float) * 2 * NU * 32 >= sizeof(float4) * 32 * SLOTS, "staging area too small");
-  static_assert(sizeof(float) * NU * 32 >= 3 * sizeof(double) * kTinyNM, "tiny-pair area too small");
+  using Smem = WarpSmem<UNLAB, NODEWISE>;
+  static_assert(sizeof(float) * 2 * NU * 32 >= sizeof(float4) * SMAX, "staging area too small");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   Smem& S = reinterpret_cast<Smem*>(smem_raw)[threadIdx.x >> 5];
-  float4* stage = reinterpret_cast<float4*>(&S.AP[0][0]);
+  float4* stage = reinterpret_cast<float4*>(&S.P[0][0]);
   const int el_dim = ds.el_dim;
+  const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
 
   for (;;) {
     unsigned long long pid = 0;
@@ -293,214 +443,141 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     if (pid >= (unsigned long long)job.npairs) break;
     int32_t ga, gb;
     decode_pair(job, (int64_t)pid, ga, gb);
-    GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
+    const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
     // orientation: L takes the graph that minimises S_U * ceil(S_L / 32)
-    int SA = 2 * A.ne, SB = 2 * B.ne;
-    long costAB = (long)SA * ((SB + 31) / 32) + A.n;  // U = A, L = B
-    long costBA = (long)SB * ((SA + 31) / 32) + B.n;
-    bool swap = (costBA < costAB) && SA <= 32 * SLOTS;
-    if (SB > 32 * SLOTS) swap = true;
+    const int SA = 2 * A.ne, SB = 2 * B.ne;
+    const long costAB = (long)SA * ((SB + 31) / 32) + A.n;  // U = A, L = B
+    const long costBA = (long)SB * ((SA + 31) / 32) + B.n;
+    const bool swap = (costBA < costAB);
     const GraphDesc U = swap ? B : A;
     const GraphDesc L = swap ? A : B;
     const int nu = U.n, m = L.n;
     const int SL = 2 * L.ne;
-    const int nslots = (SL + 31) >> 5;
+    const int ns = (SL + 31) >> 5;
 
-    // ---- prologue: octiles -> rows
-    octiles_to_rows(ds, U, lane, S.UE, S.urow, el_dim);
-    int lrow_tmp[1];
-    (void)lrow_tmp;
-    __shared__ int lrow_sh[kWarpsPerBlock][33];
-    int* lrow = lrow_sh[threadIdx.x >> 5];
-    octiles_to_rows(ds, L, lane, stage, lrow, el_dim);
-    if (nu == 0 || m == 0) { /* unreachable: n >= 1 */ }
+    // ---- prologue: octiles -> rows (U into UWL/UOFF, L staged then held in registers)
+    octiles_to_rows(ds, U, lane, S.urow, el_dim, [&](int pos, int col, float w, float lab) {
+      S.UWL[pos] = make_float2(w, lab);
+      S.UOFF[pos] = col * 128;
+    });
+    octiles_to_rows(ds, L, lane, S.lrow, el_dim, [&](int pos, int col, float w, float lab) {
+      stage[pos] = make_float4(__int_as_float(col), w, lab, 0.0f);
+    });
     __syncwarp();
-    int lcol[SLOTS];
+    int lcoff[SLOTS];
     float lw[SLOTS], llab[SLOTS];
 #pragma unroll
     for (int t = 0; t < SLOTS; ++t) {
-      int k = lane + 32 * t;
+      const int k = lane + 32 * t;
+      lcoff[t] = 0;
+      lw[t] = 0.0f;
+      llab[t] = 0.0f;
       if (k < SL) {
-        float4 e = stage[k];
-        lcol[t] = __float_as_int(e.x);
+        const float4 e = stage[k];
+        lcoff[t] = __float_as_int(e.x) * 4;
         lw[t] = e.y;
         llab[t] = e.z;
-      } else {
-        lcol[t] = 0;
-        lw[t] = 0.0f;
-        llab[t] = 0.0f;
       }
     }
     int lr0 = 0, lr1 = 0;
     if (lane < m) {
-      lr0 = lrow[lane];
-      lr1 = lrow[lane + 1];
+      lr0 = S.lrow[lane];
+      lr1 = S.lrow[lane + 1];
     }
-    if (nu * m <= kTinyNM) {
-      double val, rrt;
-      int64_t itt;
-      bool cvt;
-      double* P64 = reinterpret_cast<double*>(&S.P[0][0]);
-      float* nw = out.nodewise ? out.nodewise + out.nodewise_off[pid] : nullptr;
-      solve_tiny<EK>(ds, vk, ek, prm, U, L, S.UE, S.urow, stage, lrow, P64, P64 + kTinyNM, P64 + 2 * kTinyNM, lane,
-                     val, itt, cvt, rrt, nw, swap);
-      write_pair_outputs(out, pid, ga, gb, val, itt, cvt, rrt, lane);
-      __syncwarp();
-      continue;
-    }
-    __syncwarp();  // staging (AP/DG) is free again
 
-    // node data: L on lanes, U in shared memory
-    float ld = 1.0f, ldq = 0.0f, lp = 0.0f;
+    __syncwarp();  // staging (P/OFF) is free again
+
+    // ---- node data: L on lanes, U in shared memory; vectors as [U node][lane]
+    double ldq = 0.0;
+    float lp = 0.0f;
     if (lane < m) {
-      int64_t v = L.node_off + lane;
-      ld = (float)ds.deg[v];
-      ldq = (float)(ds.deg[v] * (double)ds.q[v]);
+      const int64_t v = L.node_off + lane;
+      ldq = ds.deg[v] * (double)ds.q[v];
       lp = ds.p[v];
     }
+    double bb_u = 0.0;
     if (lane < nu) {
-      int64_t v = U.node_off + lane;
-      S.udq[lane] = (float)(ds.deg[v] * (double)ds.q[v]);
+      const int64_t v = U.node_off + lane;
+      const double dq = ds.deg[v] * (double)ds.q[v];
+      S.udq[lane] = (float)dq;
       S.upq[lane] = ds.p[v];
-    }
-    // diag = d_i d'_i' / max(kv, v_min)  (product.py:164-178, 210)
-    const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
-    double bb_l = (lane < m) ? (double)ldq * (double)ldq : 0.0;
-    double bb_u = (lane < nu) ? (double)S.udq[lane] * (double)S.udq[lane] : 0.0;
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < NU; ++i) {
-      if (i < nu) {
-        float dg = 1.0f;
-        if (lane < m) {
-          int64_t vu = U.node_off + i, vl = L.node_off + lane;
-          float kv = 1.0f;
-          if (vlab) {
-            const float* la = ds.vlabel + vu * ds.nl_dim;
-            const float* lb = ds.vlabel + vl * ds.nl_dim;
-            kv = fmaxf(kernel_vec(vk, la, lb, ds.nl_dim, ds.nl_kind == LK_CAT), prm.v_min);
-          }
-          dg = (float)(ds.deg[vu] * (double)ld) / kv;
-        }
-        S.DG[i][lane] = dg;
-      }
+      bb_u = dq * dq;
     }
     // b = (d q) (x) (d' q');  eps = tol^2 b.b  (solver.py:69-74, 88) -- b.b is separable
-    const double bb = warp_sum(bb_u) * warp_sum(bb_l);
+    const double bb = warp_sum(bb_u) * warp_sum(ldq * ldq);
     const double eps = prm.tol2 * bb;
     const int64_t max_iter = prm.max_iter > 0 ? prm.max_iter : 10ll * nu * m;
     __syncwarp();
 
-    float r[NU], x[NU];
+    // x = 0, r = b, z = r / diag, p = z  (solver.py:91-97)
     double rho = 0.0, rr = 0.0;
-#pragma unroll
-    for (int i = 0; i < NU; ++i) {
-      x[i] = 0.0f;
-      r[i] = 0.0f;
-      if (i < nu && lane < m) {
-        r[i] = S.udq[i] * ldq;
-        float z = r[i] / S.DG[i][lane];
-        S.P[i][lane] = z;
-        rho += (double)r[i] * (double)z;
-        rr += (double)r[i] * (double)r[i];
-      } else if (i < nu) {
-        S.P[i][lane] = 0.0f;
+#pragma unroll 1
+    for (int i = 0; i < nu; ++i) {
+      float p0 = 0.0f;
+      if (lane < m) {
+        const float d = (float)diag_of(ds, vk, prm, vlab, U.node_off + i, L.node_off + lane);
+        const float r0 = (float)((double)S.udq[i] * ldq);
+        S.DG[i][lane] = d;
+        S.R[i][lane] = r0;
+        p0 = r0 * rcp_approx(d);
+        rho += (double)r0 * (double)p0;
+        rr += (double)r0 * (double)r0;
       }
+      S.P[i][lane] = p0;
+      if constexpr (NODEWISE) S.X[i][lane] = 0.0f;
     }
     rho = warp_sum(rho);
     rr = warp_sum(rr);
     bool conv = rr < eps;
     int64_t it = 0;
+    double value = 0.0;
+    const bool self_pair = (ga == gb);
+    const bool active = lane < m;
     __syncwarp();
 
     while (!conv && it < max_iter) {
-      // ---------------- XMV: AP = diag * P - offdiag(P)
-      if constexpr (UNLAB) {
-        // T[j][i'] = sum_{k' in L(i')} w' P[j][col(k')]   (P B^T)
-        for (int j = 0; j < nu; ++j) {
-          const float* prow = S.P[j];
-#pragma unroll
-          for (int t = 0; t < SLOTS; ++t)
-            if (t < nslots) S.SEG[lane + 32 * t] = lw[t] * prow[lcol[t]];
-          __syncwarp();
-          if (lane < m) {
-            float s = 0.0f;
-            for (int k = lr0; k < lr1; ++k) s += S.SEG[k];
-            S.T[j][lane] = s;
-          }
-          __syncwarp();
-        }
-        for (int i = 0; i < nu; ++i) {
-          float s = 0.0f;
-          for (int k = S.urow[i]; k < S.urow[i + 1]; ++k) {
-            float4 e = S.UE[k];
-            s = fmaf(e.y, S.T[__float_as_int(e.x)][lane], s);
-          }
-          S.AP[i][lane] = S.DG[i][lane] * S.P[i][lane] - s;
-        }
-      } else {
-        for (int i = 0; i < nu; ++i) {
-          float acc[SLOTS];
-#pragma unroll
-          for (int t = 0; t < SLOTS; ++t) acc[t] = 0.0f;
-          const int k0 = S.urow[i], k1 = S.urow[i + 1];
-          for (int k = k0; k < k1; ++k) {
-            float4 e = S.UE[k];
-            const float* prow = S.P[__float_as_int(e.x)];
-            const float wa = e.y, la = e.z;
-#pragma unroll
-            for (int t = 0; t < SLOTS; ++t) {
-              if (t < nslots) {
-                float kap = edge_kappa<EK>(ek, la, llab[t]);
-                acc[t] = fmaf(kap, wa * prow[lcol[t]], acc[t]);
-              }
-            }
-          }
-#pragma unroll
-          for (int t = 0; t < SLOTS; ++t)
-            if (t < nslots) S.SEG[lane + 32 * t] = acc[t] * lw[t];
-          __syncwarp();
-          if (lane < m) {
-            float s = 0.0f;
-            for (int k = lr0; k < lr1; ++k) s += S.SEG[k];
-            S.AP[i][lane] = S.DG[i][lane] * S.P[i][lane] - s;
-          }
-          __syncwarp();
-        }
-      }
-      __syncwarp();
-      if (ga == gb) {
+      // ---------------- off-diagonal product OFF = (A (x) A' . ke) P
+      xmv_dispatch<EK>(ns, S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);
+      if (self_pair) {
         // self pair: the exact operator maps symmetric fields to symmetric fields;
-        // symmetrising AP keeps the FP32 Krylov space in that subspace, as the
-        // reference's FP64 iteration does (iteration-count parity on the Gram diagonal)
-        float sym[NU];
-#pragma unroll
-        for (int i = 0; i < NU; ++i)
-          if (i < nu && lane < m) sym[i] = 0.5f * (S.AP[i][lane] + S.AP[lane][i]);
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < NU; ++i)
-          if (i < nu && lane < m) S.AP[i][lane] = sym[i];
+        // symmetrising keeps the FP32 Krylov space in that subspace as the FP64
+        // reference does (diag * P is exactly symmetric already)
+        for (int i = 0; i < lane && active; ++i) {
+          const float v = 0.5f * (S.OFF[i][lane] + S.OFF[lane][i]);
+          S.OFF[i][lane] = v;
+          S.OFF[lane][i] = v;
+        }
         __syncwarp();
       }
       ++it;
-      // ---------------- PCG update (solver.py:98-110)
-      double pap = 0.0;
-#pragma unroll
-      for (int i = 0; i < NU; ++i)
-        if (i < nu && lane < m) pap += (double)S.P[i][lane] * (double)S.AP[i][lane];
+      // ---------------- PCG update (solver.py:98-110); A p = diag * p - OFF
+      double pap = 0.0, pxp = 0.0;
+      if (active) {
+#pragma unroll 2
+        for (int i = 0; i < nu; ++i) {
+          const float p = S.P[i][lane];
+          const float ap = fmaf(S.DG[i][lane], p, -S.OFF[i][lane]);
+          S.OFF[i][lane] = ap;
+          pap += (double)p * (double)ap;
+          pxp += (double)S.upq[i] * (double)p;
+        }
+      }
       pap = warp_sum(pap);
+      pxp = warp_sum(pxp * (double)lp);
       const double alpha = rho / pap;
+      value += alpha * pxp;  // px . x accumulated as sum_k alpha_k (px . p_k)
       const float af = (float)alpha;
       double rr_l = 0.0, rz_l = 0.0;
-#pragma unroll
-      for (int i = 0; i < NU; ++i) {
-        if (i < nu && lane < m) {
-          x[i] = fmaf(af, S.P[i][lane], x[i]);
-          r[i] = fmaf(-af, S.AP[i][lane], r[i]);
-          float z = r[i] / S.DG[i][lane];
-          rr_l += (double)r[i] * (double)r[i];
-          rz_l += (double)r[i] * (double)z;
+      if (active) {
+#pragma unroll 2
+        for (int i = 0; i < nu; ++i) {
+          if constexpr (NODEWISE) S.X[i][lane] = fmaf(af, S.P[i][lane], S.X[i][lane]);
+          const float r = fmaf(-af, S.OFF[i][lane], S.R[i][lane]);
+          const float z = r * rcp_approx(S.DG[i][lane]);
+          S.R[i][lane] = r;
+          S.OFF[i][lane] = z;
+          rr_l += (double)r * (double)r;
+          rz_l += (double)r * (double)z;
         }
       }
       rr = warp_sum(rr_l);
@@ -510,47 +587,113 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
         break;
       }
       const float beta = (float)(rho_next / rho);
-#pragma unroll
-      for (int i = 0; i < NU; ++i) {
-        if (i < nu && lane < m) {
-          float z = r[i] / S.DG[i][lane];
-          S.P[i][lane] = fmaf(beta, S.P[i][lane], z);
-        }
+      if (active) {
+#pragma unroll 4
+        for (int i = 0; i < nu; ++i) S.P[i][lane] = fmaf(beta, S.P[i][lane], S.OFF[i][lane]);
       }
       rho = rho_next;
       __syncwarp();
     }
 
-    // ---------------- epilogue: value = px . x (solver.py:114)
-    double val = 0.0;
-#pragma unroll
-    for (int i = 0; i < NU; ++i)
-      if (i < nu && lane < m) val += (double)S.upq[i] * (double)lp * (double)x[i];
-    val = warp_sum(val);
-    if (out.nodewise) {
-      float* nw = out.nodewise + out.nodewise_off[pid];
-      // field is [n_a][n_b] with a = first graph of the pair
-#pragma unroll
-      for (int i = 0; i < NU; ++i) {
-        if (i < nu && lane < m) {
-          int64_t idx = swap ? (int64_t)lane * nu + i : (int64_t)i * m + lane;
-          nw[idx] = x[i];
+    if constexpr (NODEWISE) {
+      if (out.nodewise && active) {
+        float* nw = out.nodewise + out.nodewise_off[pid];
+        // field is [n_a][n_b] with a = first graph of the pair
+        for (int i = 0; i < nu; ++i) {
+          const int64_t idx = swap ? (int64_t)lane * nu + i : (int64_t)i * m + lane;
+          nw[idx] = S.X[i][lane];
         }
       }
     }
+    write_pair_outputs(out, pid, ga, gb, value, it, conv, rr, lane);
+    __syncwarp();
+  }
+}
+
+// Tiny-pair kernel: warp per pair, FP64 vectors (see solve_tiny).
+struct TinySmem {
+  float2 UWL[SMAX];
+  int UOFF[SMAX];
+  float4 LE[SMAX];
+  double V[3 * kTinyMax];  // P, AP, DG
+  int urow[NU + 8];
+  int lrow[40];
+};
+
+template <int EK>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
+           unsigned long long* queue) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  TinySmem& S = reinterpret_cast<TinySmem*>(smem_raw)[threadIdx.x >> 5];
+  const int el_dim = ds.el_dim;
+  for (;;) {
+    unsigned long long pid = 0;
+    if (lane == 0) pid = atomicAdd(queue, 1ull);
+    pid = __shfl_sync(0xffffffffu, pid, 0);
+    if (pid >= (unsigned long long)job.npairs) break;
+    int32_t ga, gb;
+    decode_pair(job, (int64_t)pid, ga, gb);
+    const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
+    octiles_to_rows(ds, A, lane, S.urow, el_dim, [&](int pos, int col, float w, float lab) {
+      S.UWL[pos] = make_float2(w, lab);
+      S.UOFF[pos] = col * 128;
+    });
+    octiles_to_rows(ds, B, lane, S.lrow, el_dim, [&](int pos, int col, float w, float lab) {
+      S.LE[pos] = make_float4(__int_as_float(col), w, lab, 0.0f);
+    });
+    __syncwarp();
+    double val, rr;
+    int64_t it;
+    bool conv;
+    float* nw = out.nodewise ? out.nodewise + out.nodewise_off[pid] : nullptr;
+    solve_tiny<EK>(ds, vk, ek, prm, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.V, S.V + kTinyMax,
+                   S.V + 2 * kTinyMax, lane, val, it, conv, rr, nw, false);
     write_pair_outputs(out, pid, ga, gb, val, it, conv, rr, lane);
     __syncwarp();
   }
 }
 
 template <int EK>
+static cudaError_t launch_tiny_ek(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,
+                                  const PairJob& job, const SolveParams& prm, const SolveOut& out,
+                                  unsigned long long* queue, int num_sms, cudaStream_t stream) {
+  auto kern = k_pcg_tiny<EK>;
+  const size_t smem = sizeof(TinySmem) * kWarpsPerBlock;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32, smem);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (int64_t)(per_sm < 1 ? 1 : per_sm) * num_sms;
+  const int64_t need = (job.npairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, kWarpsPerBlock * 32, smem, stream>>>(ds, vk, ek, job, prm, out, queue);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                            const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
+                            cudaStream_t stream) {
+  int kind = prm.labeled ? ek.kind : KK_NONE;
+  if (kind == KK_CONST1) kind = KK_NONE;
+  switch (kind) {
+    case KK_SE: return launch_tiny_ek<KK_SE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_DELTA: return launch_tiny_ek<KK_DELTA>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_POLY: return launch_tiny_ek<KK_POLY>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    default: return launch_tiny_ek<KK_NONE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+  }
+}
+
+template <int EK, bool NODEWISE>
 static cudaError_t launch_ek(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                              const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
                              cudaStream_t stream) {
-  constexpr int NU = SmallClass::NU, SLOTS = SmallClass::SLOTS;
-  using Smem = WarpSmem<NU, SLOTS, EK == KK_NONE>;
-  auto kern = k_pcg_warp<NU, SLOTS, EK>;
-  size_t smem = sizeof(Smem) * kWarpsPerBlock;
+  using Smem = WarpSmem<EK == KK_NONE, NODEWISE>;
+  auto kern = k_pcg_warp<EK, NODEWISE>;
+  const size_t smem = sizeof(Smem) * kWarpsPerBlock;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -558,24 +701,32 @@ static cudaError_t launch_ek(const DatasetDev& ds, const KernelDesc& vk, const K
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)per_sm * num_sms;
-  int64_t need = (job.npairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int64_t need = (job.npairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, kWarpsPerBlock * 32, smem, stream>>>(ds, vk, ek, job, prm, out, queue);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
-                            const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
-                            cudaStream_t stream) {
+template <bool NODEWISE>
+static cudaError_t launch_nw(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
+                             cudaStream_t stream) {
   int kind = prm.labeled ? ek.kind : KK_NONE;
   if (kind == KK_CONST1) kind = KK_NONE;
   switch (kind) {
-    case KK_SE: return launch_ek<KK_SE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
-    case KK_DELTA: return launch_ek<KK_DELTA>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
-    case KK_POLY: return launch_ek<KK_POLY>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
-    default: return launch_ek<KK_NONE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_SE: return launch_ek<KK_SE, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_DELTA: return launch_ek<KK_DELTA, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_POLY: return launch_ek<KK_POLY, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    default: return launch_ek<KK_NONE, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
   }
+}
+
+cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                            const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
+                            cudaStream_t stream) {
+  if (out.nodewise) return launch_nw<true>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+  return launch_nw<false>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
 }
 
 }  // namespace mgk

@@ -32,11 +32,12 @@ SIGNATURES = {
     "mgk_tiles": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P]),
     "mgk_degrees": (C.c_int, [_P, C.c_int32, _P]),
     "mgk_gram": (C.c_int, [_P, C.c_double, C.c_int64, _P, _P, _P]),
-    "mgk_gram_shard": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, _P, _P, _P, _P]),
-    "mgk_gram_assemble": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P, _P]),
+    "mgk_gram_shard": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, _P, _P, _P, _P, _P, _P]),
     "mgk_pairs": (C.c_int, [_P, C.c_int64, _P, _P, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
     "mgk_kernel": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
     "mgk_last_timing": (C.c_int, [_P, _P, _P]),
+    "mgk_bench_peaks": (C.c_int, [C.c_int, _P, _P]),
+    "mgk_transfer_bytes": (C.c_int, [_P, _P]),
 }
 
 
@@ -150,25 +151,16 @@ class Context:
         return K, it, cv.astype(bool)
 
     def gram_shard(self, rank: int, world: int, tol: float, max_iter: int = 0):
+        """This rank's share of the Gram pairs: (a, b, value, iterations, converged)."""
         n = C.c_int64()
-        check(self.lib.mgk_gram_shard(self.h, rank, world, float(tol), int(max_iter), C.byref(n), None, None, None))
-        v = np.empty(n.value, dtype=np.float64)
-        it = np.empty(n.value, dtype=np.int32)
-        cv = np.empty(n.value, dtype=np.uint8)
-        check(self.lib.mgk_gram_shard(self.h, rank, world, float(tol), int(max_iter), C.byref(n), _ptr(v), _ptr(it),
-                                      _ptr(cv)))
-        return v, it, cv
-
-    def gram_assemble(self, world: int, lens, values, iters, conv):
-        G = self.G
-        lens = np.ascontiguousarray(lens, dtype=np.int64)
-        K = np.empty((G, G), dtype=np.float64)
-        Ki = np.empty((G, G), dtype=np.int32)
-        Kc = np.empty((G, G), dtype=np.uint8)
-        check(self.lib.mgk_gram_assemble(self.h, world, _ptr(lens), _ptr(np.ascontiguousarray(values, np.float64)),
-                                         _ptr(np.ascontiguousarray(iters, np.int32)),
-                                         _ptr(np.ascontiguousarray(conv, np.uint8)), _ptr(K), _ptr(Ki), _ptr(Kc)))
-        return K, Ki, Kc.astype(bool)
+        check(self.lib.mgk_gram_shard(self.h, rank, world, float(tol), int(max_iter), C.byref(n),
+                                      None, None, None, None, None))
+        k = n.value
+        pa, pb = np.empty(k, np.int32), np.empty(k, np.int32)
+        v, it, cv = np.empty(k, np.float64), np.empty(k, np.int32), np.empty(k, np.uint8)
+        check(self.lib.mgk_gram_shard(self.h, rank, world, float(tol), int(max_iter), C.byref(n), _ptr(pa),
+                                      _ptr(pb), _ptr(v), _ptr(it), _ptr(cv)))
+        return pa, pb, v, it, cv
 
     def pairs(self, a, b, tol: float, max_iter: int = 0, nodewise: bool = False, sizes=None):
         a = np.ascontiguousarray(a, dtype=np.int32)
@@ -185,6 +177,16 @@ class Context:
         check(self.lib.mgk_pairs(self.h, k, _ptr(a), _ptr(b), float(tol), int(max_iter), _ptr(val), _ptr(it),
                                  _ptr(res), _ptr(cv), _ptr(nw)))
         return val, it, res, cv.astype(bool), nw
+
+    def peaks(self, device: int = 0):
+        f, e = C.c_double(), C.c_double()
+        check(self.lib.mgk_bench_peaks(int(device), C.byref(f), C.byref(e)))
+        return f.value, e.value
+
+    def transfer_bytes(self):
+        h, d = C.c_int64(), C.c_int64()
+        check(self.lib.mgk_transfer_bytes(C.byref(h), C.byref(d)))
+        return h.value, d.value
 
     def last_timing(self):
         ms, n = C.c_double(), C.c_int32()
