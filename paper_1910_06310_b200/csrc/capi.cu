@@ -936,8 +936,8 @@ int mgk_reorder(mgk_ctx* c, int method, uint64_t seed, int apply, int64_t* perms
   int rc = prepare(c);  // octiles of the current order drive the tile-count fallback
   if (rc) return rc;
   std::vector<int64_t> fwd;
-  rc = pbr_device(c->G, c->node_off, c->edge_off, c->ei, c->ej, seed, c->d_tiles.ptr, c->graphs, c->device, c->stream,
-                  fwd, g_err);
+  rc = pbr_device(c->G, c->node_off, c->edge_off, c->ei, c->ej, seed, c->d_tiles.ptr, c->graphs, c->d_trow.ptr,
+                  c->device, c->stream, fwd, g_err);
   if (rc) return rc;
   if (perms_out) std::copy(fwd.begin(), fwd.end(), perms_out);
   if (apply) {

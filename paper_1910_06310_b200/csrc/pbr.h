@@ -11,6 +11,7 @@ namespace mgk {
 // the dataset; returns 0 or an MGK_E_* code with the message in err.
 int pbr_device(int G, const std::vector<int64_t>& node_off, const std::vector<int64_t>& edge_off,
                const std::vector<int32_t>& ei, const std::vector<int32_t>& ej, uint64_t seed,
-               const Octile* d_tiles, const std::vector<GraphDesc>& graphs, int device, cudaStream_t stream,
+               const Octile* d_tiles, const std::vector<GraphDesc>& graphs, const int32_t* d_trow, int device,
+               cudaStream_t stream,
                std::vector<int64_t>& forward, std::string& err);
 }  // namespace mgk

@@ -164,3 +164,43 @@ def test_bindings_roundtrip(mgk):
         mgkbind.kernel(loop, loop)
     m, flags = mgkbind.gram([p2, p2], normalize=True)
     assert flags.all() and np.allclose(np.diagonal(m), 1.0)
+
+
+def test_pbr_permutations_bit_exact(mgk, golden_structure):
+    """Device PBR (csrc/pbr.cu) == reference pbr_reorder on every golden graph, seeds 0 and 3."""
+    graphs = [graph_from_json(r["graph"]) for r in golden_structure]
+    for seed in ("0", "3"):
+        perms = mgk.pbr_reorder_many(graphs, seed=int(seed))
+        for rec, perm in zip(golden_structure, perms):
+            assert perm.forward.tolist() == rec["pbr"][seed], (rec["name"], seed)
+
+
+def test_pbr_tiles_after_reorder(mgk, golden_structure):
+    for rec in golden_structure:
+        g = graph_from_json(rec["graph"])
+        perm = mgk.pbr_reorder(g, seed=0)
+        t = mgk.build_tiles(mgk.apply_permutation(g, perm))
+        assert t.tile_count == rec["pbr_tiles_0"], rec["name"]
+
+
+def test_kernel_with_pbr_reorder_golden(mgk, golden_kernels):
+    for rec in golden_kernels:
+        if rec["reorder"] != "pbr":
+            continue
+        ga, gb = graph_from_json(rec["a"]), graph_from_json(rec["b"])
+        res = mgk.kernel(ga, gb, rec["vkernel"], rec["ekernel"], reorder="pbr", seed=0)
+        assert abs(res.value - rec["value"]) <= REL * abs(rec["value"])
+        assert abs(res.iterations - rec["iterations"]) <= 1
+        nw = np.asarray(rec["nodewise"])
+        assert np.max(np.abs(res.nodewise - nw)) <= REL * np.max(np.abs(nw))
+
+
+def test_pbr_protein_shaped_vs_oracle(mgk):
+    """Shuffled C-alpha chains (config 3 shape) at n up to 200 against the oracle restatement."""
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(77)
+    graphs = [synth.protein(rng, int(n)) for n in (40, 90, 150)]
+    perms = mgk.pbr_reorder_many(graphs, seed=5)
+    for g, p in zip(graphs, perms):
+        assert p.forward.tolist() == O.pbr_reorder(g, 5).tolist()
