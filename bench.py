@@ -412,8 +412,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--count", type=int, default=7165)
-    ap.add_argument("--cpu-pairs", type=int, default=4000)
-    ap.add_argument("--ref-pairs", type=int, default=3000)
+    ap.add_argument("--cpu-pairs", type=int, default=300000)
+    ap.add_argument("--ref-pairs", type=int, default=100000)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
