@@ -208,6 +208,8 @@ struct mgk_ctx {
   DBuf<int64_t> d_gseg, d_segstart, d_segtile;
   DBuf<uint64_t> d_keys, d_keys2;
   DBuf<Octile> d_tiles;
+  DBuf<int32_t> d_rowptr, d_panel;
+  DBuf<float4> d_rowent;
   DatasetDev ds{};
   KernelDesc vk{}, ek{};
   // solver buffers
@@ -480,6 +482,7 @@ static int prepare(mgk_ctx* c) {
   }
   for (int64_t i = 0; i < ne; ++i) w32[i] = (float)c->w[i];
   std::vector<GraphDesc> gd(G);
+  std::vector<int32_t> rowptr(nn + G), panels;
   int64_t trow_off = 0;
   for (int g = 0; g < G; ++g) {
     GraphDesc d{};
@@ -490,6 +493,29 @@ static int prepare(mgk_ctx* c) {
     d.nz_off = 2 * c->edge_off[g];
     d.trow_off = trow_off;
     trow_off += ceil8(d.n) + 1;
+    // row pointers of the row-ordered octile expansion + row panels of <= kPanelCap nonzeros
+    d.rowptr_off = c->node_off[g] + g;
+    int32_t* rp = rowptr.data() + d.rowptr_off;
+    std::fill(rp, rp + d.n + 1, 0);
+    for (int64_t e = c->edge_off[g]; e < c->edge_off[g + 1]; ++e) {
+      ++rp[c->ei[e] + 1];
+      ++rp[c->ej[e] + 1];
+    }
+    d.maxdeg = 0;
+    for (int i = 0; i < d.n; ++i) {
+      d.maxdeg = std::max(d.maxdeg, rp[i + 1]);
+      rp[i + 1] += rp[i];
+    }
+    d.panel_off = (int64_t)panels.size();
+    if (d.maxdeg <= kPanelCap) {
+      panels.push_back(0);
+      for (int i = 0; i < d.n; ++i)
+        if (rp[i + 1] - rp[panels.back()] > kPanelCap) panels.push_back(i);
+      panels.push_back(d.n);
+      d.npanels = (int32_t)(panels.size() - d.panel_off - 1);
+    } else {
+      d.npanels = 0;
+    }
     gd[g] = d;
     for (int64_t i = c->node_off[g]; i < c->node_off[g + 1]; ++i) ngraph[i] = g;
     for (int64_t i = c->edge_off[g]; i < c->edge_off[g + 1]; ++i) egraph[i] = g;
@@ -504,6 +530,8 @@ static int prepare(mgk_ctx* c) {
   CUDA_TRY(c->d_ngraph.upload(ngraph, s));
   CUDA_TRY(c->d_graphs.upload(gd, s));
   CUDA_TRY(c->d_trow.alloc(trow_off));
+  CUDA_TRY(c->d_rowptr.upload(rowptr, s));
+  CUDA_TRY(c->d_panel.upload(panels, s));
   DatasetDev& ds = c->ds;
   ds = DatasetDev{};
   ds.G = G;
@@ -519,6 +547,16 @@ static int prepare(mgk_ctx* c) {
   c->ek = to_desc(c->espec);
   rc = build_octiles(c);
   if (rc) return rc;
+  // row-ordered expansion of the octiles (panel solver input)
+  CUDA_TRY(c->d_rowent.alloc(2 * ne));
+  if (ne > 0)
+    k_rows_fill<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(nn, c->d_ngraph.ptr, c->d_graphs.ptr, c->d_tiles.ptr,
+                                                              c->d_trow.ptr, c->d_nzw.ptr, c->d_nzlabel.ptr,
+                                                              c->ds.el_dim, c->d_rowptr.ptr, c->d_rowent.ptr);
+  CUDA_TRY(cudaGetLastError());
+  ds.rowptr = c->d_rowptr.ptr;
+  ds.rowent = c->d_rowent.ptr;
+  ds.panel_row = c->d_panel.ptr;
   c->prepared = true;
   return MGK_OK;
 }
@@ -583,7 +621,7 @@ static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   return p;
 }
 
-enum JobKernel { JK_BLOCK = 0, JK_WARP = 1, JK_TINY = 2 };
+enum JobKernel { JK_BLOCK = 0, JK_WARP = 1, JK_TINY = 2, JK_PANEL = 3 };
 
 struct JobSpec {
   PairJob job;
@@ -591,6 +629,19 @@ struct JobSpec {
   int64_t max_n, max_m, max_su, max_sl;
 };
 
+
+// Panel solver eligibility: scalar edge labels and row panels for every graph
+// (a row of more than kPanelCap nonzeros sends the dataset to the block kernel).
+static bool panel_dataset(const mgk_ctx* c) {
+  if (c->ds.el_dim > 1) return false;
+  if (getenv("MGK_NO_PANEL")) return false;
+  for (const GraphDesc& d : c->graphs)
+    if (2 * d.ne > 128 && d.npanels <= 0) return false;
+  return true;
+}
+
+// Largest n*m the panel solver keeps in shared memory (P and Ap: 2 n m floats).
+constexpr int64_t kPanelSmemNM = 8192;
 
 // Per-CTA slab (floats) for the block kernel.
 static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl) {
@@ -604,19 +655,32 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   cudaStream_t s = c->stream;
   CUDA_TRY(c->d_queue.alloc(std::max<size_t>(jobs.size(), 1)));
   CUDA_TRY(cudaMemsetAsync(c->d_queue.ptr, 0, std::max<size_t>(jobs.size(), 1) * sizeof(unsigned long long), s));
-  // scratch for block jobs
-  int64_t slab = 0;
-  for (auto& j : jobs)
-    if (j.kernel == JK_BLOCK && j.job.npairs > 0) slab = std::max(slab, block_slab(c, j.max_n, j.max_m, j.max_su, j.max_sl));
-  int nctas = 2 * c->num_sms;
-  if (slab > 0) {
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    int64_t budget = (int64_t)(free_b * 0.6) / 4;
-    int64_t fit = budget / slab;
-    if (fit < nctas) nctas = (int)std::max<int64_t>(fit, 1);
-    CUDA_TRY(c->d_scratch.alloc((size_t)slab * nctas));
+  // scratch slabs (block and panel jobs run one after another on the stream and share the buffer)
+  std::vector<int64_t> slabs(jobs.size(), 0);
+  std::vector<int> ctas(jobs.size(), 0), svec(jobs.size(), 0);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const int64_t budget = (int64_t)(free_b * 0.6) / 4 + (int64_t)c->d_scratch.n;
+  int64_t need = 0;
+  for (size_t k = 0; k < jobs.size(); ++k) {
+    JobSpec& j = jobs[k];
+    if (j.job.npairs <= 0) continue;
+    if (j.kernel == JK_BLOCK) {
+      slabs[k] = block_slab(c, j.max_n, j.max_m, j.max_su, j.max_sl);
+      ctas[k] = 2 * c->num_sms;
+    } else if (j.kernel == JK_PANEL) {
+      const int64_t nm = j.max_n * j.max_m;
+      slabs[k] = 5 * ((nm + 31) / 32 * 32);
+      svec[k] = (int)(2 * std::min<int64_t>(nm, kPanelSmemNM));
+      ctas[k] = panel_ctas_per_sm(svec[k]) * c->num_sms;
+    } else {
+      continue;
+    }
+    int64_t fit = std::max<int64_t>(budget / std::max<int64_t>(slabs[k], 1), 1);
+    if (fit < ctas[k]) ctas[k] = (int)fit;
+    need = std::max(need, slabs[k] * ctas[k]);
   }
+  if (need > 0) CUDA_TRY(c->d_scratch.alloc((size_t)need));
   c->last_launches = 0;
   CUDA_TRY(cudaEventRecord(c->ev0, s));
   for (size_t k = 0; k < jobs.size(); ++k) {
@@ -636,8 +700,12 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
       e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
     else if (j.kernel == JK_TINY)
       e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
+    else if (j.kernel == JK_PANEL)
+      e = launch_pcg_panel(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slabs[k],
+                           ctas[k], svec[k], s);
     else
-      e = launch_pcg_block(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slab, nctas, s);
+      e = launch_pcg_block(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slabs[k],
+                           ctas[k], s);
     if (e != cudaSuccess) return fail(MGK_E_CUDA, "solver launch failed: %s", cudaGetErrorString(e));
     ++c->last_launches;
   }
@@ -710,12 +778,13 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   jt.kernel = JK_TINY;
   JobSpec j2{};
   j2.job = PairJob{PM_TRI, (int32_t)no, 0, no * (no + 1) / 2, 0, 1, dother, nullptr, nullptr, nullptr};
-  j2.kernel = JK_BLOCK;
+  const int big = panel_dataset(c) ? JK_PANEL : JK_BLOCK;
+  j2.kernel = big;
   j2.max_n = j2.max_m = mx(other, true);
   j2.max_su = j2.max_sl = mx(other, false);
   JobSpec j3{};
   j3.job = PairJob{PM_RECT, (int32_t)no, (int32_t)ns, no * ns, 0, 1, dother, dsmall, nullptr, nullptr};
-  j3.kernel = JK_BLOCK;
+  j3.kernel = big;
   j3.max_n = mx(other, true);
   j3.max_m = mx(small, true);
   j3.max_su = mx(other, false);
@@ -849,7 +918,7 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
   jobs[1].kernel = JK_TINY;
   jobs[2].job = PairJob{PM_LIST, 0, 0, (int64_t)ba.size(), 0, 1, c->d_list_b.ptr + nw0 + nt0,
                         c->d_list_c.ptr + nw0 + nt0, nullptr, nullptr};
-  jobs[2].kernel = JK_BLOCK;
+  jobs[2].kernel = panel_dataset(c) ? JK_PANEL : JK_BLOCK;
   jobs[2].max_n = bn;
   jobs[2].max_m = bm;
   jobs[2].max_su = bsu;

@@ -16,6 +16,18 @@ namespace mgk {
 
 constexpr int kTile = 8;
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // One non-empty 8x8 block (tiles.py:23-48): bit (r%8)*8 + c%8 set per nonzero;
 // the block's values sit at nz_off .. nz_off+popc(bitmap) in ascending bit order.
 struct __align__(16) Octile {
@@ -34,8 +46,16 @@ struct GraphDesc {
   int64_t tile_off;   // into octiles
   int64_t trow_off;   // into tile-row pointer array (ceil(n/8) + 1 entries)
   int32_t ntiles;     // non-empty octiles
+  int32_t maxdeg;     // largest row length (nonzeros of one node)
+  int64_t rowptr_off; // into the row-pointer array (n + 1 entries, = node_off + graph index)
+  int64_t panel_off;  // into the panel row-boundary array (npanels + 1 entries)
+  int32_t npanels;    // row panels of <= kPanelCap nonzeros (0 if a row exceeds the cap)
   int32_t pad;
 };
+
+// Row panels (pcg_panel.cu): consecutive rows whose nonzeros fit 32 lanes x 8 slots.
+constexpr int kPanelSlots = 8;
+constexpr int kPanelCap = 32 * kPanelSlots;
 
 // Base-kernel descriptor (basekernels.py:60-172); kind codes match basekernels.py.
 enum KernelKind : int32_t { KK_CONST1 = 0, KK_DELTA = 1, KK_SE = 2, KK_POLY = 3, KK_NONE = 4 };
@@ -48,6 +68,27 @@ struct KernelDesc {
   float se_scale;      // sqrt(alpha * log2(e)): labels are pre-scaled so SE = exp2(-|a-b|^2)
   float coef[kMaxPoly];
 };
+
+
+// Edge base kernel on lowered scalar labels, specialised on the kind
+// (basekernels.py:73-172): SE labels are pre-scaled so kappa = exp2(-(a-b)^2),
+// delta labels are equivalence-class ids compared as integers.
+template <int EK>
+__device__ __forceinline__ float edge_kappa(const KernelDesc& k, float a, float b) {
+  if constexpr (EK == KK_SE) {
+    float d = a - b;
+    return ex2_approx(-d * d);
+  } else if constexpr (EK == KK_DELTA) {
+    return (__float_as_int(a) == __float_as_int(b)) ? 1.0f : k.h;
+  } else if constexpr (EK == KK_POLY) {
+    float d = fabsf(a - b);
+    float acc = 0.0f;
+    for (int c = k.ncoef - 1; c >= 0; --c) acc = fmaf(acc, d, k.coef[c]);
+    return fminf(fmaxf(acc, 0.0f), 1.0f);
+  } else {
+    return 1.0f;
+  }
+}
 
 // Label storage kinds (graphs.py:126-146).
 enum LabelKind : int32_t { LK_NONE = 0, LK_CAT = 1, LK_VEC = 2 };
@@ -69,6 +110,10 @@ struct DatasetDev {
   const int32_t* trow;         // tile-row pointers, relative to the graph's tile_off
   const float* nz_w;           // [sum S]
   const float* nz_label;       // [sum S * el_dim]
+  // row-ordered expansion of the octiles (built on the device once per dataset)
+  const int32_t* rowptr;       // [sum (n + 1)] relative to the graph's nz base
+  const float4* rowent;        // [sum S] {col (int bits), w, label0, 0} ascending column per row
+  const int32_t* panel_row;    // [sum (npanels + 1)] first row of every panel
 };
 
 __host__ __device__ inline int ceil8(int n) { return (n + 7) >> 3; }

@@ -97,6 +97,8 @@ __global__ void k_degrees(int64_t, const int32_t*, const GraphDesc*, const Octil
                           const float*, const double*, double*);
 __global__ void k_scan_exclusive(int64_t, const int32_t*, int64_t*);
 __global__ void k_trow(int, const int64_t*, const int64_t*, GraphDesc*, int32_t*);
+__global__ void k_rows_fill(int64_t, const int32_t*, const GraphDesc*, const Octile*, const int32_t*, const float*,
+                            const float*, int, const int32_t*, float4*);
 constexpr int kSortSmemBytes = 8192 * 8;
 
 // ---- solvers (pcg_warp.cu, pcg_block.cu)
@@ -112,6 +114,12 @@ cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const Ke
 cudaError_t launch_pcg_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                             int num_sms, cudaStream_t stream);
+// panel class (pcg_panel.cu): CTA per pair, any size whose lane graph has row panels
+cudaError_t launch_pcg_panel(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
+                             float* scratch, int64_t scratch_floats_per_cta, int nctas, int smem_vec_floats,
+                             cudaStream_t stream);
+int panel_ctas_per_sm(int smem_vec_floats);
 cudaError_t launch_pcg_block(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                              const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                              float* scratch, int64_t scratch_floats_per_cta, int nctas, cudaStream_t stream);

@@ -47,13 +47,17 @@ struct PbrScratch {
   int* ec;       // k*k
   int* sizes;    // k
   int* targets;  // k
+  unsigned* adjbits;  // k x W   bit Q of row P: ec[P][Q] > 0 (P != Q), W = ceil(k / 32)
+  unsigned* elig;     // W       destination parts allowed for the current move
   int* stack;    // 6k   recursion tasks (begin, end, first_part, nparts)
   int* dbg;      // 2n   candidates before FM refinement (parity triage)
 };
 
+__host__ __device__ inline int pbr_words(int k) { return (k + 31) >> 5; }
+
 __host__ __device__ inline int64_t pbr_scratch_ints(int n, int S, int k) {
   return (int64_t)(n + 1) + S + n + 2 * n + n + n + n + n + 2 * n + n + 4 * n + (int64_t)n * k + (int64_t)k * k + k +
-         k + 6 * (int64_t)k + 2 * (int64_t)n + 64;
+         k + (int64_t)k * pbr_words(k) + pbr_words(k) + 6 * (int64_t)k + 2 * (int64_t)n + 64;
 }
 
 __device__ PbrScratch carve(int* base, int n, int S, int k) {
@@ -74,6 +78,8 @@ __device__ PbrScratch carve(int* base, int n, int S, int k) {
   s.ec = p; p += (int64_t)k * k;
   s.sizes = p; p += k;
   s.targets = p; p += k;
+  s.adjbits = reinterpret_cast<unsigned*>(p); p += (int64_t)k * pbr_words(k);
+  s.elig = reinterpret_cast<unsigned*>(p); p += pbr_words(k);
   s.stack = p;
   p += 6 * k;
   s.dbg = p;
@@ -320,6 +326,17 @@ __device__ long long ec_objective(const PbrScratch& s, int k, long long* redll) 
   return block_sum_i64(c, redll);
 }
 
+// adjacency bit (P, Q) <- ec[P][Q] > 0 (diagonal never stored; it never enters a gain)
+__device__ __forceinline__ void sync_adjbit(const PbrScratch& s, int k, int P, int Q) {
+  if (P == Q) return;
+  const unsigned bit = 1u << (Q & 31);
+  unsigned* wp = s.adjbits + (int64_t)P * pbr_words(k) + (Q >> 5);
+  if (s.ec[(int64_t)P * k + Q] > 0)
+    atomicOr(wp, bit);
+  else
+    atomicAnd(wp, ~bit);
+}
+
 __device__ void fm_move(PbrScratch& s, int k, int u, int dst) {
   const int src = s.parts[u];
   for (int q = s.rowptr[u] + threadIdx.x; q < s.rowptr[u + 1]; q += blockDim.x) {
@@ -333,8 +350,97 @@ __device__ void fm_move(PbrScratch& s, int k, int u, int dst) {
     atomicAdd(&s.conn[(int64_t)v * k + dst], 1);
   }
   __syncthreads();
+  for (int q = s.rowptr[u] + threadIdx.x; q < s.rowptr[u + 1]; q += blockDim.x) {
+    const int p = s.parts[s.adj[q]];
+    sync_adjbit(s, k, src, p);
+    sync_adjbit(s, k, p, src);
+    sync_adjbit(s, k, dst, p);
+    sync_adjbit(s, k, p, dst);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) s.parts[u] = dst;
   __syncthreads();
+}
+
+// Best move of node u under the reference's literal gain (reorder.py:171-189),
+// as a packed first-max key (0: no allowed destination).  Restated so that the
+// k destinations need not be scanned one by one:
+//   NP = parts holding a neighbour of u (may include A = part(u)),
+//   L  = sum_{P in NP, P != A} [ec[A][P] == conn[u][P]]        (the lose sum)
+//   B in NP \ {A}: the formula term by term, with the saturating OR
+//       appear = OR_{P in NP, P != B} [ec[B][P] == 0] - [pos A and ec[B][A] == 0];
+//   B not in NP, B != A: conn[u][B] = 0 collapses the formula to
+//       gain = L - OR_{P in NP} [ec[B][P] == 0]
+//     (posA, ec[A][B] > 0: dab = 0, appear = OR;  posA, ec[A][B] = 0: dab = -1 and
+//      the OR is 1 through P = A, appear = 0;  not posA: dab = 0, appear = OR),
+//     so the best such B is the lowest allowed part adjacent to every part of NP
+//     (gain L), else the lowest allowed part outside NP (gain L - 1).
+// Ties keep the lowest B, as the flat row-major argmax does.
+__device__ unsigned long long fm_node_key(const PbrScratch& s, int k, int u) {
+  const int W = pbr_words(k);
+  const int A = s.parts[u];
+  const int* cu = s.conn + (int64_t)u * k;
+  const int* ecA = s.ec + (int64_t)A * k;
+  int np[kNPMax];
+  int nnp = 0;
+  for (int q = s.rowptr[u]; q < s.rowptr[u + 1]; ++q) {
+    const int P = s.parts[s.adj[q]];
+    bool seen = false;
+    for (int t = 0; t < nnp; ++t) seen |= (np[t] == P);
+    if (!seen && nnp < kNPMax) np[nnp++] = P;
+  }
+  int L = 0;
+  for (int t = 0; t < nnp; ++t) {
+    const int P = np[t];
+    L += (P != A && ecA[P] == cu[P]);
+  }
+  const bool posA = cu[A] > 0;
+  auto allowed = [&](int B) { return (s.elig[B >> 5] >> (B & 31)) & 1u; };
+  int bestg = -(1 << 20), bestB = k;
+  for (int t = 0; t < nnp; ++t) {
+    const int B = np[t];
+    if (B == A || !allowed(B)) continue;
+    const int cuB = cu[B];
+    const int loseB = (cuB > 0 && ecA[B] == cuB) ? 1 : 0;
+    const int new_ab = ecA[B] - cuB + cu[A];
+    const int dab = (ecA[B] > 0 ? 1 : 0) - (new_ab > 0 ? 1 : 0);
+    const unsigned* adjB = s.adjbits + (int64_t)B * W;
+    int orv = 0;
+    for (int t2 = 0; t2 < nnp && !orv; ++t2) {
+      const int P = np[t2];
+      orv = (P != B && !((adjB[P >> 5] >> (P & 31)) & 1u)) ? 1 : 0;
+    }
+    const int appear = orv - ((posA && !((adjB[A >> 5] >> (A & 31)) & 1u)) ? 1 : 0);
+    const int g = L - loseB + dab - appear;
+    if (g > bestg || (g == bestg && B < bestB)) {
+      bestg = g;
+      bestB = B;
+    }
+  }
+  int f0 = -1, f1 = -1;
+  for (int w = 0; w < W && f0 < 0; ++w) {
+    unsigned base = s.elig[w];
+    if ((A >> 5) == w) base &= ~(1u << (A & 31));
+    for (int t = 0; t < nnp; ++t)
+      if ((np[t] >> 5) == w) base &= ~(1u << (np[t] & 31));
+    if (!base) continue;
+    if (f1 < 0) f1 = w * 32 + __ffs(base) - 1;
+    unsigned m0 = base;
+    for (int t = 0; t < nnp && m0; ++t) m0 &= s.adjbits[(int64_t)np[t] * W + w];
+    if (m0) f0 = w * 32 + __ffs(m0) - 1;
+  }
+  int fg = L, fB = f0;
+  if (f0 < 0) {
+    fg = L - 1;
+    fB = f1;
+  }
+  if (fB >= 0 && (fg > bestg || (fg == bestg && fB < bestB))) {
+    bestg = fg;
+    bestB = fB;
+  }
+  if (bestB >= k) return 0ull;
+  const unsigned long long flat = (unsigned long long)u * k + bestB;
+  return ((unsigned long long)(bestg + (1ll << 20)) << 40) | ((1ull << 40) - 1 - flat);
 }
 
 __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned long long* red64, long long* redll,
@@ -357,6 +463,17 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
     }
   }
   __syncthreads();
+  const int W = pbr_words(k);
+  for (int64_t x = threadIdx.x; x < (int64_t)k * W; x += blockDim.x) {
+    const int P = (int)(x / W), w = (int)(x - (int64_t)P * W);
+    unsigned word = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int Q = w * 32 + b;
+      if (Q < k && Q != P && s.ec[(int64_t)P * k + Q] > 0) word |= 1u << b;
+    }
+    s.adjbits[x] = word;
+  }
+  __syncthreads();
   for (int pass = 0; pass < kMaxPasses; ++pass) {
     for (int p = threadIdx.x; p < k; p += blockDim.x) s.sizes[p] = 0;
     __syncthreads();
@@ -376,6 +493,16 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
       long long devbad = 0;
       for (int p = threadIdx.x; p < k; p += blockDim.x) devbad += s.sizes[p] != s.targets[p];
       const bool balanced = block_sum_i64(devbad, redll) == 0;
+      // allowed destinations: every part when balanced, else the undersized ones
+      for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        unsigned word = 0;
+        for (int b = 0; b < 32; ++b) {
+          const int B = w * 32 + b;
+          if (B < k && (balanced || s.sizes[B] < s.targets[B])) word |= 1u << b;
+        }
+        s.elig[w] = word;
+      }
+      __syncthreads();
       unsigned long long key = 0;
       for (int attempt = 0; attempt < 2 && key == 0; ++attempt) {
         const bool ignore_locks = attempt == 1;
@@ -384,46 +511,8 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
           if (!ignore_locks && s.locked[u]) continue;
           const int A = s.parts[u];
           if (!balanced && !(s.sizes[A] > s.targets[A])) continue;
-          const int* cu = s.conn + (int64_t)u * k;
-          const int* ecA = s.ec + (int64_t)A * k;
-          // distinct neighbour parts of u (ascending adjacency order)
-          int np[kNPMax];
-          int nnp = 0;
-          for (int q = s.rowptr[u]; q < s.rowptr[u + 1]; ++q) {
-            const int P = s.parts[s.adj[q]];
-            bool seen = false;
-            for (int t = 0; t < nnp; ++t) seen |= (np[t] == P);
-            if (!seen && nnp < kNPMax) np[nnp++] = P;
-          }
-          // lose[P] = pos[P] & ec[A][P] == conn[u][P], lose[A] = 0
-          int lose_sum = 0;
-          for (int t = 0; t < nnp; ++t) {
-            const int P = np[t];
-            lose_sum += (P != A && ecA[P] == cu[P]);
-          }
-          const bool posA = cu[A] > 0;
-          for (int B = 0; B < k; ++B) {
-            if (B == A) continue;
-            if (!balanced && !(s.sizes[B] < s.targets[B])) continue;
-            const int cuB = cu[B];
-            const int loseB = (cuB > 0 && ecA[B] == cuB) ? 1 : 0;
-            const int new_ab = ecA[B] - cuB + cu[A];
-            const int dab = (ecA[B] > 0 ? 1 : 0) - (new_ab > 0 ? 1 : 0);
-            // appear = OR_P(pos[P] & ez[B][P]) - pos[A] & ez[B][A]   (saturating OR, reorder.py:183-184)
-            const int* ecB = s.ec + (int64_t)B * k;
-            int orv = 0;
-            for (int t = 0; t < nnp && !orv; ++t) {
-              const int P = np[t];
-              orv = (P != B && ecB[P] == 0) ? 1 : 0;
-            }
-            const int appear = orv - ((posA && B != A && ecB[A] == 0) ? 1 : 0);
-            const long long gain = (long long)lose_sum - loseB + dab - appear;
-            // first max in row-major (u, B) order
-            const unsigned long long flat = (unsigned long long)u * k + B;
-            const unsigned long long kk = ((unsigned long long)(gain + (1ll << 20)) << 40) |
-                                          ((1ull << 40) - 1 - flat);
-            key = kk > key ? kk : key;
-          }
+          const unsigned long long kk = fm_node_key(s, k, u);
+          key = kk > key ? kk : key;
         }
         key = block_max_u64(key, red64);
       }

@@ -1,0 +1,451 @@
+// K3 + K4 (panel class): one CTA solves one graph pair of any size.
+//
+// Replaces, per pair, ProductOperator.__init__ (product.py:184-222), apply /
+// apply_offdiag (product.py:351-419) and solve_pcg (solver.py:77-121) for the
+// pairs the warp solver cannot hold in one warp (configs 3-5: 24 < n <= 5000).
+//
+// Same on-the-fly XMV as pcg_warp.cu, generalised from "the whole lane graph in
+// one warp's registers" to row panels: the lane graph L is cut (once per
+// dataset, on the host from the degree sequence) into panels of consecutive
+// rows holding at most 256 nonzeros; a warp holds one panel in registers
+// (lane l owns panel nonzeros l + 32 t, t < NS) and walks a chunk of U rows:
+//
+//   acc[t]  = sum_{k in U(i)} kappa(e_k, e'_t) w_k P[j_k][col_L(t)]
+//   OFF[i][r] = sum_{t in L(r)} acc[t] w'_t          (segment sum in shared memory)
+//   AP[i][r]  = diag[i][r] P[i][r] - OFF[i][r]
+//
+// Every (panel, U-row chunk) item writes a disjoint block of AP, so there are
+// no atomics and the result is independent of the warp schedule.  Small lane
+// graphs (S_L <= 64 / 128) use a single panel with 2 / 4 slots per lane.
+//
+// PCG state: P and AP live in shared memory when 2 n m floats fit the per-CTA
+// budget chosen at launch (mid-size pairs), otherwise in a per-CTA slab in HBM
+// (read through L1/L2; the gathers P[j][col] of one warp touch a narrow column
+// window of a few rows, which is what the PBR ordering buys).  R, diag and the
+// nodewise iterate always sit in the slab (streamed once per iteration).
+// Dot products are FP64 block reductions in a fixed order (deterministic).
+#include "mgk_internal.h"
+
+namespace mgk {
+
+constexpr int kPT = 256;          // threads per CTA
+constexpr int kPW = kPT / 32;     // warps per CTA
+constexpr int kSegFloats = 2 * kPanelCap;  // per-warp segment buffer (two U rows)
+constexpr int kPanelStaticSmem = kPW * kSegFloats * 4;
+
+__device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  if (lane == 0) buf[w] = v;
+  __syncthreads();
+  double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < kPW; ++k) {
+    s.x += buf[k].x;
+    s.y += buf[k].y;
+  }
+  return s;
+}
+
+// acc[t] += sum_{k in [k0, k1)} kappa(e_k, e'_t) w_k P[j_k][lcol[t]]   (U row, warp-uniform)
+template <int NS, int EK>
+__device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float4* __restrict__ ue, int k0, int k1,
+                                               const float* P, int m, const int (&lcol)[NS],
+                                               const float (&llab)[NS], float (&acc)[NS]) {
+  int k = k0;
+  for (; k + 1 < k1; k += 2) {
+    const float4 e0 = ue[k], e1 = ue[k + 1];
+    const float* r0 = P + __float_as_int(e0.x) * m;
+    const float* r1 = P + __float_as_int(e1.x) * m;
+    float p0[NS], p1[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      p0[t] = r0[lcol[t]];
+      p1[t] = r1[lcol[t]];
+    }
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      acc[t] = fmaf(edge_kappa<EK>(ek, e0.z, llab[t]), e0.y * p0[t], acc[t]);
+      acc[t] = fmaf(edge_kappa<EK>(ek, e1.z, llab[t]), e1.y * p1[t], acc[t]);
+    }
+  }
+  if (k < k1) {
+    const float4 e0 = ue[k];
+    const float* r0 = P + __float_as_int(e0.x) * m;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) acc[t] = fmaf(edge_kappa<EK>(ek, e0.z, llab[t]), e0.y * r0[lcol[t]], acc[t]);
+  }
+}
+
+struct PairView {
+  const int32_t* urp;   // U row pointers (relative to ue)
+  const float4* ue;     // U row entries
+  const int32_t* lrp;
+  const float4* le;
+  const int32_t* prow;  // L panel row boundaries (null: single panel = all rows)
+  int n, m, np, rpc;
+};
+
+// AP = diag * P - XMV(P) over all (panel, chunk) items of this warp.
+template <int NS, int EK>
+__device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float* P, float* AP, const float* DG,
+                           float* SEG, int lane, int warp) {
+  const int n = v.n, m = v.m;
+  const int nchunks = (n + v.rpc - 1) / v.rpc;
+  const int items = v.np * nchunks;
+  for (int item = warp; item < items; item += kPW) {
+    const int p = item % v.np, c = item / v.np;
+    const int rbeg = v.prow ? v.prow[p] : 0;
+    const int rend = v.prow ? v.prow[p + 1] : m;
+    const int kbeg = v.lrp[rbeg], kend = v.lrp[rend];
+    int lcol[NS];
+    float lw[NS], llab[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const int k = kbeg + lane + 32 * t;
+      lcol[t] = 0;
+      lw[t] = 0.0f;
+      llab[t] = 0.0f;
+      if (k < kend) {
+        const float4 e = v.le[k];
+        lcol[t] = __float_as_int(e.x);
+        lw[t] = e.y;
+        llab[t] = e.z;
+      }
+    }
+    // this lane's first two panel rows, cached
+    const int ra = rbeg + lane, rb = rbeg + lane + 32;
+    int qa0 = 0, qa1 = 0, qb0 = 0, qb1 = 0;
+    if (ra < rend) {
+      qa0 = v.lrp[ra] - kbeg;
+      qa1 = v.lrp[ra + 1] - kbeg;
+    }
+    if (rb < rend) {
+      qb0 = v.lrp[rb] - kbeg;
+      qb1 = v.lrp[rb + 1] - kbeg;
+    }
+    const int i0 = c * v.rpc, i1 = min(n, i0 + v.rpc);
+    for (int i = i0; i < i1; i += 2) {
+      const bool two = i + 1 < i1;
+      float acc0[NS], acc1[NS];
+#pragma unroll
+      for (int t = 0; t < NS; ++t) acc0[t] = acc1[t] = 0.0f;
+      row_accumulate<NS, EK>(ek, v.ue, v.urp[i], v.urp[i + 1], P, m, lcol, llab, acc0);
+      if (two) row_accumulate<NS, EK>(ek, v.ue, v.urp[i + 1], v.urp[i + 2], P, m, lcol, llab, acc1);
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        SEG[lane + 32 * t] = acc0[t] * lw[t];
+        SEG[kPanelCap + lane + 32 * t] = acc1[t] * lw[t];
+      }
+      __syncwarp();
+      const int base = i * m;
+      for (int r = ra; r < rend; r += 32) {
+        int q0, q1;
+        if (r == ra) {
+          q0 = qa0;
+          q1 = qa1;
+        } else if (r == rb) {
+          q0 = qb0;
+          q1 = qb1;
+        } else {
+          q0 = v.lrp[r] - kbeg;
+          q1 = v.lrp[r + 1] - kbeg;
+        }
+        float s0 = 0.0f, s1 = 0.0f;
+        for (int q = q0; q < q1; ++q) {
+          s0 += SEG[q];
+          s1 += SEG[kPanelCap + q];
+        }
+        const int e0 = base + r;
+        AP[e0] = fmaf(DG[e0], P[e0], -s0);
+        if (two) AP[e0 + m] = fmaf(DG[e0 + m], P[e0 + m], -s1);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Lane-side cost of a graph (slot-rounded nonzeros a warp streams per U nonzero).
+__device__ __forceinline__ int64_t lane_cost(const GraphDesc& g) {
+  const int S = 2 * g.ne;
+  if (S <= 64) return 64;
+  if (S <= 128) return 128;
+  if (g.npanels <= 0) return (int64_t)1 << 40;
+  return (int64_t)g.npanels * kPanelCap;
+}
+
+template <int EK, bool NODEWISE>
+__global__ void __launch_bounds__(kPT, 2)
+k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
+            unsigned long long* queue, float* scratch, int64_t slab, int smem_vec) {
+  extern __shared__ __align__(16) float psm[];
+  __shared__ double2 red[2][kPW];
+  __shared__ unsigned long long sh_pid;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* SEG = psm + warp * kSegFloats;
+  float* svec = psm + kPW * kSegFloats;
+  const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
+  const int64_t vstride = slab / 5;
+
+  for (;;) {
+    if (threadIdx.x == 0) sh_pid = atomicAdd(queue, 1ull);
+    __syncthreads();
+    const unsigned long long pid = sh_pid;
+    if (pid >= (unsigned long long)job.npairs) break;
+    int32_t ga, gb;
+    decode_pair(job, (int64_t)pid, ga, gb);
+    const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
+    // orientation: L is the graph with the cheaper lane side (fewest streamed slots)
+    const int64_t costAB = (int64_t)(2 * A.ne) * lane_cost(B) + A.n;
+    const int64_t costBA = (int64_t)(2 * B.ne) * lane_cost(A) + B.n;
+    const bool swap = costBA < costAB;
+    const GraphDesc U = swap ? B : A;
+    const GraphDesc L = swap ? A : B;
+    const int n = U.n, m = L.n, nm = n * m;
+    const int SL = 2 * L.ne;
+    const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : 8);
+
+    PairView v;
+    v.urp = ds.rowptr + U.rowptr_off;
+    v.ue = ds.rowent + U.nz_off;
+    v.lrp = ds.rowptr + L.rowptr_off;
+    v.le = ds.rowent + L.nz_off;
+    v.prow = ns == 8 ? ds.panel_row + L.panel_off : nullptr;
+    v.n = n;
+    v.m = m;
+    v.np = ns == 8 ? L.npanels : 1;
+    {
+      int rpc = (n * v.np) / (4 * kPW);
+      rpc = rpc < 2 ? 2 : (rpc > 32 ? 32 : rpc);
+      v.rpc = (rpc + 1) & ~1;
+    }
+
+    float* base = scratch + (int64_t)blockIdx.x * slab;
+    float* R = base;
+    float* DG = base + vstride;
+    float* X = base + 2 * vstride;
+    float* P = base + 3 * vstride;
+    float* AP = base + 4 * vstride;
+    if (2 * nm <= smem_vec) {
+      P = svec;
+      AP = svec + nm;
+    }
+    const int di = kPT / m, dl = kPT % m;
+
+    // ---- setup (solver.py:69-74, 91-97): diag, b, x = 0, r = b, z = r / diag, p = z
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = threadIdx.x; i < n; i += kPT) {
+      const double dq = ds.deg[U.node_off + i] * (double)ds.q[U.node_off + i];
+      acc.x += dq * dq;
+    }
+    for (int i = threadIdx.x; i < m; i += kPT) {
+      const double dq = ds.deg[L.node_off + i] * (double)ds.q[L.node_off + i];
+      acc.y += dq * dq;
+    }
+    int flip = 0;
+    double2 s = block_sum2(acc, red[flip]);
+    flip ^= 1;
+    const double eps = prm.tol2 * s.x * s.y;
+    acc = make_double2(0.0, 0.0);
+    {
+      int i = threadIdx.x / m, l = threadIdx.x % m;
+      for (int e = threadIdx.x; e < nm; e += kPT) {
+        const int64_t vu = U.node_off + i, vl = L.node_off + l;
+        float kv = 1.0f;
+        if (vlab)
+          kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
+                                ds.nl_kind == LK_CAT), prm.v_min);
+        const float dg = (float)(ds.deg[vu] * ds.deg[vl] / (double)kv);
+        const float b = (float)((ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]));
+        const float z = b * rcp_approx(dg);
+        DG[e] = dg;
+        R[e] = b;
+        P[e] = z;
+        if constexpr (NODEWISE) X[e] = 0.0f;
+        acc.x += (double)b * (double)z;
+        acc.y += (double)b * (double)b;
+        l += dl;
+        i += di;
+        if (l >= m) {
+          l -= m;
+          ++i;
+        }
+      }
+    }
+    s = block_sum2(acc, red[flip]);
+    flip ^= 1;
+    double rho = s.x, rr = s.y;
+    bool conv = rr < eps;
+    const int64_t max_iter = prm.max_iter > 0 ? prm.max_iter : 10ll * nm;
+    int64_t it = 0;
+    double value = 0.0;
+    const bool self_pair = (ga == gb);
+    __syncthreads();
+
+    while (!conv && it < max_iter) {
+      switch (ns) {
+        case 2: xmv_panels<2, EK>(ek, v, P, AP, DG, SEG, lane, warp); break;
+        case 4: xmv_panels<4, EK>(ek, v, P, AP, DG, SEG, lane, warp); break;
+        default: xmv_panels<8, EK>(ek, v, P, AP, DG, SEG, lane, warp); break;
+      }
+      __syncthreads();
+      if (self_pair) {
+        // self pair: keep the iterate exactly symmetric (see pcg_warp.cu)
+        for (int e = threadIdx.x; e < nm; e += kPT) {
+          const int i = e / m, l = e - i * m;
+          if (i < l) {
+            const int f = l * m + i;
+            const float a = AP[e], b = AP[f];
+            const float sym = 0.5f * (a + b);
+            AP[e] = sym;
+            AP[f] = sym;
+          }
+        }
+        __syncthreads();
+      }
+      ++it;
+      // pass 1: p.Ap and px.p (value = sum_k alpha_k px.p_k)
+      acc = make_double2(0.0, 0.0);
+      {
+        int i = threadIdx.x / m, l = threadIdx.x % m;
+        for (int e = threadIdx.x; e < nm; e += kPT) {
+          const float p = P[e];
+          acc.x += (double)p * (double)AP[e];
+          acc.y += (double)(ds.p[U.node_off + i] * ds.p[L.node_off + l]) * (double)p;
+          l += dl;
+          i += di;
+          if (l >= m) {
+            l -= m;
+            ++i;
+          }
+        }
+      }
+      s = block_sum2(acc, red[flip]);
+      flip ^= 1;
+      const double alpha = rho / s.x;
+      value += alpha * s.y;
+      const float af = (float)alpha;
+      // pass 2: x += alpha p, r -= alpha Ap, z = r / diag (stored over Ap)
+      acc = make_double2(0.0, 0.0);
+      for (int e = threadIdx.x; e < nm; e += kPT) {
+        if constexpr (NODEWISE) X[e] = fmaf(af, P[e], X[e]);
+        const float r = fmaf(-af, AP[e], R[e]);
+        const float z = r * rcp_approx(DG[e]);
+        R[e] = r;
+        AP[e] = z;
+        acc.x += (double)r * (double)r;
+        acc.y += (double)r * (double)z;
+      }
+      s = block_sum2(acc, red[flip]);
+      flip ^= 1;
+      rr = s.x;
+      const double rho_next = s.y;
+      if (rr < eps) {
+        conv = true;
+        break;
+      }
+      const float beta = (float)(rho_next / rho);
+      for (int e = threadIdx.x; e < nm; e += kPT) P[e] = fmaf(beta, P[e], AP[e]);
+      rho = rho_next;
+      __syncthreads();
+    }
+
+    if constexpr (NODEWISE) {
+      if (out.nodewise) {
+        float* nw = out.nodewise + out.nodewise_off[pid];
+        int i = threadIdx.x / m, l = threadIdx.x % m;
+        for (int e = threadIdx.x; e < nm; e += kPT) {
+          nw[swap ? l * n + i : e] = X[e];
+          l += dl;
+          i += di;
+          if (l >= m) {
+            l -= m;
+            ++i;
+          }
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      if (out.value) out.value[pid] = value;
+      if (out.iters) out.iters[pid] = (int32_t)it;
+      if (out.conv) out.conv[pid] = conv ? 1 : 0;
+      if (out.residual) out.residual[pid] = (float)sqrt(rr);
+      if (out.pair_a) out.pair_a[pid] = ga;
+      if (out.pair_b) out.pair_b[pid] = gb;
+      const double kval = conv ? value : __longlong_as_double(0x7ff8000000000000ll);
+      if (out.K) {
+        out.K[(int64_t)ga * out.G + gb] = kval;
+        out.K[(int64_t)gb * out.G + ga] = kval;
+      }
+      if (out.K_iters) {
+        out.K_iters[(int64_t)ga * out.G + gb] = (int32_t)it;
+        out.K_iters[(int64_t)gb * out.G + ga] = (int32_t)it;
+      }
+      if (out.K_conv) {
+        out.K_conv[(int64_t)ga * out.G + gb] = conv;
+        out.K_conv[(int64_t)gb * out.G + ga] = conv;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int EK, bool NODEWISE>
+static cudaError_t launch_panel_ek(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,
+                                   const PairJob& job, const SolveParams& prm, const SolveOut& out,
+                                   unsigned long long* queue, float* scratch, int64_t slab, int nctas, int smem_vec,
+                                   cudaStream_t stream) {
+  auto kern = k_pcg_panel<EK, NODEWISE>;
+  const size_t smem = kPanelStaticSmem + (size_t)smem_vec * 4;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<nctas, kPT, smem, stream>>>(ds, vk, ek, job, prm, out, queue, scratch, slab, smem_vec);
+  return cudaGetLastError();
+}
+
+int panel_ctas_per_sm(int smem_vec) {
+  int per_sm = 0;
+  const size_t smem = kPanelStaticSmem + (size_t)smem_vec * 4;
+  cudaFuncSetAttribute(k_pcg_panel<KK_SE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_panel<KK_SE, false>, kPT, smem) != cudaSuccess)
+    return 1;
+  return per_sm < 1 ? 1 : per_sm;
+}
+
+template <bool NODEWISE>
+static cudaError_t launch_panel_nw(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,
+                                   const PairJob& job, const SolveParams& prm, const SolveOut& out,
+                                   unsigned long long* queue, float* scratch, int64_t slab, int nctas, int smem_vec,
+                                   cudaStream_t stream) {
+  int kind = prm.labeled ? ek.kind : KK_NONE;
+  if (kind == KK_CONST1) kind = KK_NONE;
+  switch (kind) {
+    case KK_SE:
+      return launch_panel_ek<KK_SE, NODEWISE>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec, stream);
+    case KK_DELTA:
+      return launch_panel_ek<KK_DELTA, NODEWISE>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec,
+                                                 stream);
+    case KK_POLY:
+      return launch_panel_ek<KK_POLY, NODEWISE>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec,
+                                                stream);
+    default:
+      return launch_panel_ek<KK_NONE, NODEWISE>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec,
+                                                stream);
+  }
+}
+
+cudaError_t launch_pcg_panel(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue, float* scratch,
+                             int64_t slab, int nctas, int smem_vec, cudaStream_t stream) {
+  if ((int64_t)nctas > job.npairs) nctas = (int)job.npairs;
+  if (nctas < 1) return cudaSuccess;
+  if (out.nodewise)
+    return launch_panel_nw<true>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec, stream);
+  return launch_panel_nw<false>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec, stream);
+}
+
+}  // namespace mgk

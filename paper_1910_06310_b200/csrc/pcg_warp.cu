@@ -59,35 +59,6 @@ struct WarpSmem {
   float udq[NU];          // d_i q_i of U nodes
 };
 
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-template <int EK>
-__device__ __forceinline__ float edge_kappa(const KernelDesc& k, float a, float b) {
-  if constexpr (EK == KK_SE) {
-    float d = a - b;
-    return ex2_approx(-d * d);
-  } else if constexpr (EK == KK_DELTA) {
-    return (__float_as_int(a) == __float_as_int(b)) ? 1.0f : k.h;
-  } else if constexpr (EK == KK_POLY) {
-    float d = fabsf(a - b);
-    float acc = 0.0f;
-    for (int c = k.ncoef - 1; c >= 0; --c) acc = fmaf(acc, d, k.coef[c]);
-    return fminf(fmaxf(acc, 0.0f), 1.0f);
-  } else {
-    return 1.0f;
-  }
-}
-
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

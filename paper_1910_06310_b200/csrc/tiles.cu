@@ -222,4 +222,31 @@ __global__ void k_trow(int G, const int64_t* __restrict__ gseg, const int64_t* _
   graphs[gidx] = g;
 }
 
+// Row-ordered expansion of the octiles for the panel solver: node i's nonzeros
+// (ascending column, the order its tile row implies) land at
+// rowent[nz_off + rowptr[i] ..].  Thread per node.
+__global__ void k_rows_fill(int64_t ntotal, const int32_t* __restrict__ node_graph, const GraphDesc* __restrict__ graphs,
+                            const Octile* __restrict__ tiles, const int32_t* __restrict__ trow,
+                            const float* __restrict__ nz_w, const float* __restrict__ nz_label, int el_dim,
+                            const int32_t* __restrict__ rowptr, float4* __restrict__ rowent) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= ntotal) return;
+  const GraphDesc g = graphs[node_graph[v]];
+  const int i = (int)(v - g.node_off);
+  const int I = i >> 3, r = i & 7;
+  const int32_t* tr = trow + g.trow_off;
+  float4* dst = rowent + g.nz_off + rowptr[g.rowptr_off + i];
+  int pos = 0;
+  for (int t = tr[I]; t < tr[I + 1]; ++t) {
+    const Octile o = tiles[g.tile_off + t];
+    uint32_t byte = (uint32_t)(o.bitmap >> (8 * r)) & 0xffu;
+    const int64_t base = g.nz_off + o.nz_off + __popcll(o.bitmap & ((1ull << (8 * r)) - 1ull));
+    for (int c = 0; byte; ++c, byte &= byte - 1) {
+      const int64_t k = base + c;
+      const float lab = el_dim > 0 ? nz_label[k * el_dim] : 0.0f;
+      dst[pos++] = make_float4(__int_as_float(o.col * 8 + (__ffs(byte) - 1)), nz_w[k], lab, 0.0f);
+    }
+  }
+}
+
 }  // namespace mgk

@@ -129,18 +129,71 @@ def test_config2_sample_vs_oracle(mgk):
         assert abs(int(res.iterations[a, b]) - o.iterations) <= 1
 
 
-def test_medium_pairs_block_kernel(mgk):
-    # graphs above the warp class (n > 24) go through the CTA-per-pair kernel
+def _medium_molecules():
     from paper_1910_06310_b200 import synth
 
     rng = np.random.default_rng(5)
-    ds = [synth.molecule(rng, int(n)) for n in (30, 45, 12, 60)]
-    res = mgk.compute_gram(ds, "delta:0.5", "se:1.0")
-    for a in range(4):
-        for b in range(a, 4):
-            o = O.solve_pcg(ds[a], ds[b], ("delta", 0.5), ("se", 1.0))
-            assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value), (a, b)
-            assert abs(int(res.iterations[a, b]) - o.iterations) <= 1
+    return [synth.molecule(rng, int(n)) for n in (30, 45, 12, 60, 100)]
+
+
+def _check_gram_vs_oracle(mgk, ds, vspec=("delta", 0.5), espec=("se", 1.0), tol=1e-10):
+    res = mgk.compute_gram(ds, "delta:0.5" if vspec else None, "se:1.0" if espec else None,
+                           mgk.SolverConfig(tolerance=tol))
+    for a in range(len(ds)):
+        for b in range(a, len(ds)):
+            o = O.solve_pcg(ds[a], ds[b], vspec, espec, tol=tol)
+            assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value), (a, b, res.matrix[a, b], o.value)
+            assert abs(int(res.iterations[a, b]) - o.iterations) <= 1, (a, b)
+
+
+def test_medium_pairs_panel_kernel(mgk):
+    # graphs above the warp class (n > 24) go through the CTA-per-pair panel kernel
+    # (pcg_panel.cu): self pairs, small x medium (orientation swap), medium x medium
+    _check_gram_vs_oracle(mgk, _medium_molecules())
+
+
+def test_medium_pairs_block_kernel(mgk, monkeypatch):
+    # the generic CTA kernel (pcg_block.cu) stays the path for vector edge labels
+    monkeypatch.setenv("MGK_NO_PANEL", "1")
+    _check_gram_vs_oracle(mgk, _medium_molecules()[:4])
+
+
+def test_panel_protein_pairs_vs_oracle(mgk):
+    """Config-3 shapes (shuffled C-alpha chains, several 256-nonzero row panels per graph)."""
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(31)
+    ds = [synth.protein(rng, int(n)) for n in (120, 200, 240)]
+    ds = [mgk.apply_permutation(g, mgk.pbr_reorder(g, seed=0)) for g in ds]
+    _check_gram_vs_oracle(mgk, ds)
+
+
+def test_panel_nodewise_vs_oracle(mgk):
+    """Nodewise field through the panel kernel, both orientations (U/L swap transposes on write)."""
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(8)
+    big = synth.protein(rng, 90)
+    small = synth.molecule(rng, 9)
+    mid = synth.molecule(rng, 40)
+    for ga, gb in ((big, small), (small, big), (mid, big), (big, big)):
+        k = mgk.kernel(ga, gb, "delta:0.5", "se:1.0")
+        o = O.solve_pcg(ga, gb, ("delta", 0.5), ("se", 1.0))
+        assert abs(k.value - o.value) <= REL * abs(o.value)
+        assert abs(k.iterations - o.iterations) <= 1
+        assert k.nodewise.shape == o.nodewise.shape
+        assert np.max(np.abs(k.nodewise - o.nodewise)) <= REL * np.max(np.abs(o.nodewise))
+
+
+def test_panel_unlabeled_rgg_vs_oracle(mgk):
+    """Config-4 shape (random geometric graphs, unlabeled, tol 1e-6 per SURVEY H1) at reduced n."""
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(4)
+    ds = [synth.rgg(rng, int(n), d) for n, d in ((150, 8), (220, 16), (180, 4))]
+    ds = [mgk.LabeledGraph.from_arrays(g.node_count, g.edges_i, g.edges_j, g.weights, default_q=0.05)
+          for g in ds]
+    _check_gram_vs_oracle(mgk, ds, None, None, tol=1e-6)
 
 
 def test_validation_errors(mgk):
