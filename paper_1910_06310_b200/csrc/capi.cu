@@ -218,7 +218,8 @@ struct mgk_ctx {
   DBuf<double> d_K, d_value;
   DBuf<int32_t> d_Kit, d_iters;
   DBuf<uint8_t> d_Kconv, d_conv;
-  DBuf<float> d_resid, d_scratch, d_nodewise;
+  DBuf<float> d_resid, d_scratch, d_nodewise, d_gridvec;
+  DBuf<double2> d_gridbuf;
   DBuf<int64_t> d_nwoff;
   DBuf<int32_t> d_pa, d_pb, d_rowcol;
   DBuf<int64_t> d_rowpre;
@@ -621,7 +622,7 @@ static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   return p;
 }
 
-enum JobKernel { JK_BLOCK = 0, JK_WARP = 1, JK_TINY = 2, JK_PANEL = 3 };
+enum JobKernel { JK_BLOCK = 0, JK_WARP = 1, JK_TINY = 2, JK_PANEL = 3, JK_GRID = 4 };
 
 struct JobSpec {
   PairJob job;
@@ -642,6 +643,13 @@ static bool panel_dataset(const mgk_ctx* c) {
 
 // Largest n*m the panel solver keeps in shared memory (P and Ap: 2 n m floats).
 constexpr int64_t kPanelSmemNM = 8192;
+// Graphs with at least large_n() nodes pair with each other on the whole device
+// (grid class); explicit pair lists use n*m >= large_n()^2.  MGK_GRID_N
+// overrides the threshold (tests drive the grid path at oracle-sized graphs).
+static int large_n() {
+  const char* t = getenv("MGK_GRID_N");
+  return t ? atoi(t) : 1024;
+}
 
 // Per-CTA slab (floats) for the block kernel.
 static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl) {
@@ -681,6 +689,14 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     need = std::max(need, slabs[k] * ctas[k]);
   }
   if (need > 0) CUDA_TRY(c->d_scratch.alloc((size_t)need));
+  int64_t grid_vstride = 0;
+  const int gblocks = grid_blocks(c->num_sms);
+  for (auto& j : jobs)
+    if (j.kernel == JK_GRID && j.job.npairs > 0) grid_vstride = std::max(grid_vstride, (j.max_n * j.max_m + 31) / 32 * 32);
+  if (grid_vstride > 0) {
+    CUDA_TRY(c->d_gridvec.alloc((size_t)(5 * grid_vstride)));
+    CUDA_TRY(c->d_gridbuf.alloc((size_t)(2 * gblocks)));
+  }
   c->last_launches = 0;
   CUDA_TRY(cudaEventRecord(c->ev0, s));
   for (size_t k = 0; k < jobs.size(); ++k) {
@@ -700,6 +716,9 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
       e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
     else if (j.kernel == JK_TINY)
       e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
+    else if (j.kernel == JK_GRID)
+      e = launch_pcg_grid(c->ds, c->vk, c->ek, j.job, prm, o, c->d_gridvec.ptr, grid_vstride, c->d_gridbuf.ptr,
+                          gblocks, s);
     else if (j.kernel == JK_PANEL)
       e = launch_pcg_panel(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slabs[k],
                            ctas[k], svec[k], s);
@@ -724,8 +743,17 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
 //   [warp kernel, FP32] and a tiny ragged job [tiny kernel, FP64];
 //   pairs with a larger graph: TRI(other) + RECT(other x small) [block kernel].
 static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
-  std::vector<int32_t> small, other;
-  for (int g = 0; g < c->G; ++g) (small_graph(c, c->graphs[g]) ? small : other).push_back(g);
+  std::vector<int32_t> small, mid, large;
+  const bool panel = panel_dataset(c);
+  for (int g = 0; g < c->G; ++g) {
+    const GraphDesc& d = c->graphs[g];
+    if (small_graph(c, d))
+      small.push_back(g);
+    else if (panel && d.n >= large_n())
+      large.push_back(g);
+    else
+      mid.push_back(g);
+  }
   auto by_size = [c](int32_t a, int32_t b) {
     const GraphDesc &x = c->graphs[a], &y = c->graphs[b];
     if (x.n != y.n) return x.n > y.n;
@@ -733,28 +761,28 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
     return a < b;
   };
   std::stable_sort(small.begin(), small.end(), by_size);
-  std::stable_sort(other.begin(), other.end(), by_size);
-  const int64_t ns = (int64_t)small.size(), no = (int64_t)other.size();
+  std::stable_sort(mid.begin(), mid.end(), by_size);
+  std::stable_sort(large.begin(), large.end(), by_size);
+  const int64_t ns = (int64_t)small.size(), nmid = (int64_t)mid.size(), nl = (int64_t)large.size();
   const int T = tiny_nm();
   // ragged rows over the size-sorted small list
   std::vector<int64_t> mpre(ns + 1, 0), tpre(ns + 1, 0);
   std::vector<int32_t> mcol(ns), tcol(ns);
-  int64_t cu = ns;  // c(u) is non-decreasing in u (n descending)
   int64_t v = 0;
   for (int64_t u = 0; u < ns; ++u) {
     const int64_t nu = c->graphs[small[u]].n;
     while (v < ns && (int64_t)c->graphs[small[v]].n * nu > T) ++v;
-    cu = v;
-    const int64_t split = std::max<int64_t>(u, cu);
+    const int64_t split = std::max<int64_t>(u, v);
     mcol[u] = (int32_t)u;
     mpre[u + 1] = mpre[u] + (split - u);
     tcol[u] = (int32_t)split;
     tpre[u + 1] = tpre[u] + (ns - split);
   }
   cudaStream_t s = c->stream;
-  std::vector<int32_t> lists;  // small then other
+  std::vector<int32_t> lists;  // small, mid, large
   lists.insert(lists.end(), small.begin(), small.end());
-  lists.insert(lists.end(), other.begin(), other.end());
+  lists.insert(lists.end(), mid.begin(), mid.end());
+  lists.insert(lists.end(), large.begin(), large.end());
   CUDA_TRY(c->d_list_a.upload(lists, s));
   std::vector<int64_t> pre(mpre);
   pre.insert(pre.end(), tpre.begin(), tpre.end());
@@ -763,12 +791,35 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   CUDA_TRY(c->d_rowpre.upload(pre, s));
   CUDA_TRY(c->d_rowcol.upload(col, s));
   const int32_t* dsmall = c->d_list_a.ptr;
-  const int32_t* dother = c->d_list_a.ptr + small.size();
+  const int32_t* dmid = dsmall + ns;
+  const int32_t* dlarge = dmid + nmid;
   auto mx = [c](const std::vector<int32_t>& vv, bool nodes) {
     int64_t r = 0;
     for (int32_t g : vv) r = std::max<int64_t>(r, nodes ? c->graphs[g].n : 2 * c->graphs[g].ne);
     return r;
   };
+  auto tri = [&](const std::vector<int32_t>& l, const int32_t* dl, int kernel) {
+    JobSpec j{};
+    const int64_t n = (int64_t)l.size();
+    j.job = PairJob{PM_TRI, (int32_t)n, 0, n * (n + 1) / 2, 0, 1, dl, nullptr, nullptr, nullptr};
+    j.kernel = kernel;
+    j.max_n = j.max_m = mx(l, true);
+    j.max_su = j.max_sl = mx(l, false);
+    return j;
+  };
+  auto rect = [&](const std::vector<int32_t>& la, const int32_t* da, const std::vector<int32_t>& lb,
+                  const int32_t* db, int kernel) {
+    JobSpec j{};
+    j.job = PairJob{PM_RECT, (int32_t)la.size(), (int32_t)lb.size(), (int64_t)la.size() * (int64_t)lb.size(), 0, 1,
+                    da, db, nullptr, nullptr};
+    j.kernel = kernel;
+    j.max_n = mx(la, true);
+    j.max_m = mx(lb, true);
+    j.max_su = mx(la, false);
+    j.max_sl = mx(lb, false);
+    return j;
+  };
+  const int cta = panel ? JK_PANEL : JK_BLOCK;
   JobSpec jm{};
   jm.job = PairJob{PM_RAGGED, (int32_t)ns, 0, mpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr, c->d_rowcol.ptr};
   jm.kernel = JK_WARP;
@@ -776,20 +827,9 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   jt.job = PairJob{PM_RAGGED, (int32_t)ns, 0, tpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr + ns + 1,
                    c->d_rowcol.ptr + ns};
   jt.kernel = JK_TINY;
-  JobSpec j2{};
-  j2.job = PairJob{PM_TRI, (int32_t)no, 0, no * (no + 1) / 2, 0, 1, dother, nullptr, nullptr, nullptr};
-  const int big = panel_dataset(c) ? JK_PANEL : JK_BLOCK;
-  j2.kernel = big;
-  j2.max_n = j2.max_m = mx(other, true);
-  j2.max_su = j2.max_sl = mx(other, false);
-  JobSpec j3{};
-  j3.job = PairJob{PM_RECT, (int32_t)no, (int32_t)ns, no * ns, 0, 1, dother, dsmall, nullptr, nullptr};
-  j3.kernel = big;
-  j3.max_n = mx(other, true);
-  j3.max_m = mx(small, true);
-  j3.max_su = mx(other, false);
-  j3.max_sl = mx(small, false);
-  jobs = {j2, j3, jm, jt};  // big pairs first (longest job first across classes)
+  // big pairs first (longest job first across classes)
+  jobs = {tri(large, dlarge, JK_GRID), rect(large, dlarge, mid, dmid, cta), rect(large, dlarge, small, dsmall, cta),
+          tri(mid, dmid, cta), rect(mid, dmid, small, dsmall, cta), jm, jt};
   return MGK_OK;
 }
 
@@ -878,9 +918,10 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
     if (a[k] < 0 || a[k] >= c->G || b[k] < 0 || b[k] >= c->G)
       return fail(MGK_E_INVALID, "pair %lld references unknown graph", (long long)k);
   // split into tiny / warp-class / block-class pairs; outputs in job order, remapped below
-  std::vector<int32_t> ta, tb, wa, wb, ba, bb;
-  std::vector<int64_t> tidx, widx, bidx;
-  int64_t bn = 0, bm = 0, bsu = 0, bsl = 0;
+  std::vector<int32_t> ta, tb, wa, wb, ba, bb, ga_, gb_;
+  std::vector<int64_t> tidx, widx, bidx, gidx;
+  int64_t bn = 0, bm = 0, bsu = 0, bsl = 0, gn = 0, gm = 0;
+  const bool panel = panel_dataset(c);
   const int T = tiny_nm();
   for (int64_t k = 0; k < npairs; ++k) {
     const GraphDesc &A = c->graphs[a[k]], &B = c->graphs[b[k]];
@@ -889,6 +930,12 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
       (tiny ? ta : wa).push_back(a[k]);
       (tiny ? tb : wb).push_back(b[k]);
       (tiny ? tidx : widx).push_back(k);
+    } else if (panel && (int64_t)A.n * B.n >= (int64_t)large_n() * large_n()) {
+      ga_.push_back(a[k]);
+      gb_.push_back(b[k]);
+      gidx.push_back(k);
+      gn = std::max<int64_t>(gn, A.n);
+      gm = std::max<int64_t>(gm, B.n);
     } else {
       ba.push_back(a[k]);
       bb.push_back(b[k]);
@@ -904,26 +951,35 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
   lb.insert(lb.end(), tb.begin(), tb.end());
   la.insert(la.end(), ba.begin(), ba.end());
   lb.insert(lb.end(), bb.begin(), bb.end());
+  la.insert(la.end(), ga_.begin(), ga_.end());
+  lb.insert(lb.end(), gb_.begin(), gb_.end());
   std::vector<int64_t> order(widx);
   order.insert(order.end(), tidx.begin(), tidx.end());
   order.insert(order.end(), bidx.begin(), bidx.end());
+  order.insert(order.end(), gidx.begin(), gidx.end());
   cudaStream_t s = c->stream;
   CUDA_TRY(c->d_list_b.upload(la, s));
   CUDA_TRY(c->d_list_c.upload(lb, s));
   const int64_t nw0 = (int64_t)wa.size(), nt0 = (int64_t)ta.size();
-  std::vector<JobSpec> jobs(3);
+  std::vector<JobSpec> jobs(4);
   jobs[0].job = PairJob{PM_LIST, 0, 0, nw0, 0, 1, c->d_list_b.ptr, c->d_list_c.ptr, nullptr, nullptr};
   jobs[0].kernel = JK_WARP;
   jobs[1].job = PairJob{PM_LIST, 0, 0, nt0, 0, 1, c->d_list_b.ptr + nw0, c->d_list_c.ptr + nw0, nullptr, nullptr};
   jobs[1].kernel = JK_TINY;
   jobs[2].job = PairJob{PM_LIST, 0, 0, (int64_t)ba.size(), 0, 1, c->d_list_b.ptr + nw0 + nt0,
                         c->d_list_c.ptr + nw0 + nt0, nullptr, nullptr};
-  jobs[2].kernel = panel_dataset(c) ? JK_PANEL : JK_BLOCK;
+  jobs[2].kernel = panel ? JK_PANEL : JK_BLOCK;
   jobs[2].max_n = bn;
   jobs[2].max_m = bm;
   jobs[2].max_su = bsu;
   jobs[2].max_sl = bsl;
-  std::vector<int64_t> offs = {0, nw0, nw0 + nt0};
+  const int64_t nb0 = (int64_t)ba.size();
+  jobs[3].job = PairJob{PM_LIST, 0, 0, (int64_t)ga_.size(), 0, 1, c->d_list_b.ptr + nw0 + nt0 + nb0,
+                        c->d_list_c.ptr + nw0 + nt0 + nb0, nullptr, nullptr};
+  jobs[3].kernel = JK_GRID;
+  jobs[3].max_n = gn;
+  jobs[3].max_m = gm;
+  std::vector<int64_t> offs = {0, nw0, nw0 + nt0, nw0 + nt0 + nb0};
   CUDA_TRY(c->d_value.alloc(npairs));
   CUDA_TRY(c->d_iters.alloc(npairs));
   CUDA_TRY(c->d_conv.alloc(npairs));

@@ -120,6 +120,11 @@ cudaError_t launch_pcg_panel(const DatasetDev& ds, const KernelDesc& vk, const K
                              float* scratch, int64_t scratch_floats_per_cta, int nctas, int smem_vec_floats,
                              cudaStream_t stream);
 int panel_ctas_per_sm(int smem_vec_floats);
+// grid class (pcg_panel.cu): one pair at a time on the whole device (cooperative launch)
+cudaError_t launch_pcg_grid(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                            const SolveParams& prm, const SolveOut& out, float* vec, int64_t vstride, double2* gbuf,
+                            int nblocks, cudaStream_t stream);
+int grid_blocks(int num_sms);
 cudaError_t launch_pcg_block(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                              const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                              float* scratch, int64_t scratch_floats_per_cta, int nctas, cudaStream_t stream);

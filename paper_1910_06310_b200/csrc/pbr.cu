@@ -24,7 +24,7 @@
 
 namespace mgk {
 
-constexpr int kPbrThreads = 256;
+constexpr int kPbrThreads = 512;
 constexpr int kPbrWarps = kPbrThreads / 32;
 constexpr int kMaxPasses = 10;
 constexpr int kNPMax = 128;  // distinct neighbour parts tracked per node in a gain evaluation

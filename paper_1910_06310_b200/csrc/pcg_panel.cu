@@ -24,9 +24,13 @@
 // window of a few rows, which is what the PBR ordering buys).  R, diag and the
 // nodewise iterate always sit in the slab (streamed once per iteration).
 // Dot products are FP64 block reductions in a fixed order (deterministic).
+#include <cooperative_groups.h>
+
 #include "mgk_internal.h"
 
 namespace mgk {
+
+namespace cg = cooperative_groups;
 
 constexpr int kPT = 256;          // threads per CTA
 constexpr int kPW = kPT / 32;     // warps per CTA
@@ -90,15 +94,19 @@ struct PairView {
   int n, m, np, rpc;
 };
 
-// AP = diag * P - XMV(P) over all (panel, chunk) items of this warp.
+// AP = diag * P - XMV(P) over the (panel, chunk) items w0, w0 + wstride, ...
+// When part != nullptr the warp also accumulates (p.Ap, px.p) over the
+// elements it wrote (every element is written by exactly one item).
 template <int NS, int EK>
 __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float* P, float* AP, const float* DG,
-                           float* SEG, int lane, int warp) {
+                           float* SEG, int lane, int64_t w0, int64_t wstride, const float* pu, const float* pl,
+                           double2* part) {
   const int n = v.n, m = v.m;
   const int nchunks = (n + v.rpc - 1) / v.rpc;
-  const int items = v.np * nchunks;
-  for (int item = warp; item < items; item += kPW) {
-    const int p = item % v.np, c = item / v.np;
+  const int64_t items = (int64_t)v.np * nchunks;
+  double pap = 0.0, pxp = 0.0;
+  for (int64_t item = w0; item < items; item += wstride) {
+    const int p = (int)(item / nchunks), c = (int)(item - (int64_t)p * nchunks);
     const int rbeg = v.prow ? v.prow[p] : 0;
     const int rend = v.prow ? v.prow[p + 1] : m;
     const int kbeg = v.lrp[rbeg], kend = v.lrp[rend];
@@ -120,13 +128,16 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
     // this lane's first two panel rows, cached
     const int ra = rbeg + lane, rb = rbeg + lane + 32;
     int qa0 = 0, qa1 = 0, qb0 = 0, qb1 = 0;
+    float pla = 0.0f, plb = 0.0f;
     if (ra < rend) {
       qa0 = v.lrp[ra] - kbeg;
       qa1 = v.lrp[ra + 1] - kbeg;
+      if (part) pla = pl[ra];
     }
     if (rb < rend) {
       qb0 = v.lrp[rb] - kbeg;
       qb1 = v.lrp[rb + 1] - kbeg;
+      if (part) plb = pl[rb];
     }
     const int i0 = c * v.rpc, i1 = min(n, i0 + v.rpc);
     for (int i = i0; i < i1; i += 2) {
@@ -143,17 +154,26 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
       }
       __syncwarp();
       const int base = i * m;
+      float pu0 = 0.0f, pu1 = 0.0f;
+      if (part) {
+        pu0 = pu[i];
+        pu1 = two ? pu[i + 1] : 0.0f;
+      }
       for (int r = ra; r < rend; r += 32) {
         int q0, q1;
+        float plr;
         if (r == ra) {
           q0 = qa0;
           q1 = qa1;
+          plr = pla;
         } else if (r == rb) {
           q0 = qb0;
           q1 = qb1;
+          plr = plb;
         } else {
           q0 = v.lrp[r] - kbeg;
           q1 = v.lrp[r + 1] - kbeg;
+          plr = part ? pl[r] : 0.0f;
         }
         float s0 = 0.0f, s1 = 0.0f;
         for (int q = q0; q < q1; ++q) {
@@ -161,11 +181,40 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
           s1 += SEG[kPanelCap + q];
         }
         const int e0 = base + r;
-        AP[e0] = fmaf(DG[e0], P[e0], -s0);
-        if (two) AP[e0 + m] = fmaf(DG[e0 + m], P[e0 + m], -s1);
+        const float p0 = P[e0];
+        const float a0 = fmaf(DG[e0], p0, -s0);
+        AP[e0] = a0;
+        if (part) {
+          pap += (double)p0 * (double)a0;
+          pxp += (double)(pu0 * plr) * (double)p0;
+        }
+        if (two) {
+          const float p1 = P[e0 + m];
+          const float a1 = fmaf(DG[e0 + m], p1, -s1);
+          AP[e0 + m] = a1;
+          if (part) {
+            pap += (double)p1 * (double)a1;
+            pxp += (double)(pu1 * plr) * (double)p1;
+          }
+        }
       }
       __syncwarp();
     }
+  }
+  if (part) {
+    part->x += pap;
+    part->y += pxp;
+  }
+}
+
+template <int EK>
+__device__ __forceinline__ void xmv_dispatch(int ns, const KernelDesc& ek, const PairView& v, const float* P,
+                                             float* AP, const float* DG, float* SEG, int lane, int64_t w0,
+                                             int64_t wstride, const float* pu, const float* pl, double2* part) {
+  switch (ns) {
+    case 2: xmv_panels<2, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
+    case 4: xmv_panels<4, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
+    default: xmv_panels<8, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
   }
 }
 
@@ -287,11 +336,9 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     __syncthreads();
 
     while (!conv && it < max_iter) {
-      switch (ns) {
-        case 2: xmv_panels<2, EK>(ek, v, P, AP, DG, SEG, lane, warp); break;
-        case 4: xmv_panels<4, EK>(ek, v, P, AP, DG, SEG, lane, warp); break;
-        default: xmv_panels<8, EK>(ek, v, P, AP, DG, SEG, lane, warp); break;
-      }
+      double2 part = make_double2(0.0, 0.0);
+      xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, warp, kPW, ds.p + U.node_off, ds.p + L.node_off,
+                       self_pair ? nullptr : &part);
       __syncthreads();
       if (self_pair) {
         // self pair: keep the iterate exactly symmetric (see pcg_warp.cu)
@@ -306,16 +353,12 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
           }
         }
         __syncthreads();
-      }
-      ++it;
-      // pass 1: p.Ap and px.p (value = sum_k alpha_k px.p_k)
-      acc = make_double2(0.0, 0.0);
-      {
+        // pass 1: p.Ap and px.p (value = sum_k alpha_k px.p_k)
         int i = threadIdx.x / m, l = threadIdx.x % m;
         for (int e = threadIdx.x; e < nm; e += kPT) {
           const float p = P[e];
-          acc.x += (double)p * (double)AP[e];
-          acc.y += (double)(ds.p[U.node_off + i] * ds.p[L.node_off + l]) * (double)p;
+          part.x += (double)p * (double)AP[e];
+          part.y += (double)(ds.p[U.node_off + i] * ds.p[L.node_off + l]) * (double)p;
           l += dl;
           i += di;
           if (l >= m) {
@@ -324,7 +367,9 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
           }
         }
       }
-      s = block_sum2(acc, red[flip]);
+      ++it;
+      // lanes of a warp hold partial sums: fold them into the block reduction
+      s = block_sum2(part, red[flip]);
       flip ^= 1;
       const double alpha = rho / s.x;
       value += alpha * s.y;
@@ -446,6 +491,300 @@ cudaError_t launch_pcg_panel(const DatasetDev& ds, const KernelDesc& vk, const K
   if (out.nodewise)
     return launch_panel_nw<true>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec, stream);
   return launch_panel_nw<false>(ds, vk, ek, job, prm, out, queue, scratch, slab, nctas, smem_vec, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Grid class: one pair at a time on the whole GPU (cooperative launch), for
+// product systems too large for one SM (config 4: n up to 5000, n m up to
+// 2.5e7).  Same XMV items, strided over every warp of the grid; the PCG dot
+// products are grid reductions (per-block partials summed in block order by
+// every block after a grid barrier, so all blocks agree bit for bit).
+// ---------------------------------------------------------------------------
+__device__ double2 grid_sum2(double2 v, double2* gbuf, double2* wred, double2* sres, cg::grid_group& grid) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  if (lane == 0) wred[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 b = make_double2(0.0, 0.0);
+    for (int k = 0; k < kPW; ++k) {
+      b.x += wred[k].x;
+      b.y += wred[k].y;
+    }
+    gbuf[blockIdx.x] = b;
+  }
+  grid.sync();
+  if (w == 0) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+      const double2 x = gbuf[b];
+      t.x += x.x;
+      t.y += x.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+      t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+    }
+    if (lane == 0) *sres = t;
+  }
+  __syncthreads();
+  return *sres;
+}
+
+template <int EK, bool NODEWISE>
+__global__ void __launch_bounds__(kPT, 2)
+k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out, float* vec,
+           int64_t vstride, double2* gbuf) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) float psm[];
+  __shared__ double2 wred[kPW];
+  __shared__ double2 sres;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* SEG = psm + warp * kSegFloats;
+  const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
+  const int64_t gtid = (int64_t)blockIdx.x * kPT + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * kPT;
+  const int64_t gw = gtid >> 5, GW = gthreads >> 5;
+  float* R = vec;
+  float* DG = vec + vstride;
+  float* X = vec + 2 * vstride;
+  float* P = vec + 3 * vstride;
+  float* AP = vec + 4 * vstride;
+  int flip = 0;
+  auto gsum = [&](double2 v) {
+    double2 r = grid_sum2(v, gbuf + flip * gridDim.x, wred, &sres, grid);
+    flip ^= 1;
+    return r;
+  };
+
+  for (int64_t pid = 0; pid < job.npairs; ++pid) {
+    int32_t ga, gb;
+    decode_pair(job, pid, ga, gb);
+    const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
+    const int64_t costAB = (int64_t)(2 * A.ne) * lane_cost(B) + A.n;
+    const int64_t costBA = (int64_t)(2 * B.ne) * lane_cost(A) + B.n;
+    const bool swap = costBA < costAB;
+    const GraphDesc U = swap ? B : A;
+    const GraphDesc L = swap ? A : B;
+    const int n = U.n, m = L.n, nm = n * m;
+    const int SL = 2 * L.ne;
+    const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : 8);
+    PairView v;
+    v.urp = ds.rowptr + U.rowptr_off;
+    v.ue = ds.rowent + U.nz_off;
+    v.lrp = ds.rowptr + L.rowptr_off;
+    v.le = ds.rowent + L.nz_off;
+    v.prow = ns == 8 ? ds.panel_row + L.panel_off : nullptr;
+    v.n = n;
+    v.m = m;
+    v.np = ns == 8 ? L.npanels : 1;
+    v.rpc = 8;
+    const int64_t di = gthreads / m, dl = gthreads % m;
+
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t i = gtid; i < n; i += gthreads) {
+      const double dq = ds.deg[U.node_off + i] * (double)ds.q[U.node_off + i];
+      acc.x += dq * dq;
+    }
+    for (int64_t i = gtid; i < m; i += gthreads) {
+      const double dq = ds.deg[L.node_off + i] * (double)ds.q[L.node_off + i];
+      acc.y += dq * dq;
+    }
+    double2 s = gsum(acc);
+    const double eps = prm.tol2 * s.x * s.y;
+    acc = make_double2(0.0, 0.0);
+    {
+      int64_t i = gtid / m, l = gtid % m;
+      for (int64_t e = gtid; e < nm; e += gthreads) {
+        const int64_t vu = U.node_off + i, vl = L.node_off + l;
+        float kv = 1.0f;
+        if (vlab)
+          kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
+                                ds.nl_kind == LK_CAT), prm.v_min);
+        const float dg = (float)(ds.deg[vu] * ds.deg[vl] / (double)kv);
+        const float b = (float)((ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]));
+        const float z = b * rcp_approx(dg);
+        DG[e] = dg;
+        R[e] = b;
+        P[e] = z;
+        if constexpr (NODEWISE) X[e] = 0.0f;
+        acc.x += (double)b * (double)z;
+        acc.y += (double)b * (double)b;
+        l += dl;
+        i += di;
+        if (l >= m) {
+          l -= m;
+          ++i;
+        }
+      }
+    }
+    s = gsum(acc);
+    double rho = s.x, rr = s.y;
+    bool conv = rr < eps;
+    const int64_t max_iter = prm.max_iter > 0 ? prm.max_iter : 10ll * nm;
+    int64_t it = 0;
+    double value = 0.0;
+    const bool self_pair = (ga == gb);
+
+    while (!conv && it < max_iter) {
+      double2 part = make_double2(0.0, 0.0);
+      xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, gw, GW, ds.p + U.node_off, ds.p + L.node_off,
+                       self_pair ? nullptr : &part);
+      if (self_pair) {
+        grid.sync();
+        for (int64_t e = gtid; e < nm; e += gthreads) {
+          const int i = (int)(e / m), l = (int)(e - (int64_t)i * m);
+          if (i < l) {
+            const int f = l * m + i;
+            const float a = AP[e], b = AP[f];
+            const float sym = 0.5f * (a + b);
+            AP[e] = sym;
+            AP[f] = sym;
+          }
+        }
+        grid.sync();
+        int64_t i = gtid / m, l = gtid % m;
+        for (int64_t e = gtid; e < nm; e += gthreads) {
+          const float p = P[e];
+          part.x += (double)p * (double)AP[e];
+          part.y += (double)(ds.p[U.node_off + i] * ds.p[L.node_off + l]) * (double)p;
+          l += dl;
+          i += di;
+          if (l >= m) {
+            l -= m;
+            ++i;
+          }
+        }
+      }
+      ++it;
+      s = gsum(part);
+      const double alpha = rho / s.x;
+      value += alpha * s.y;
+      const float af = (float)alpha;
+      acc = make_double2(0.0, 0.0);
+      for (int64_t e = gtid; e < nm; e += gthreads) {
+        if constexpr (NODEWISE) X[e] = fmaf(af, P[e], X[e]);
+        const float r = fmaf(-af, AP[e], R[e]);
+        const float z = r * rcp_approx(DG[e]);
+        R[e] = r;
+        AP[e] = z;
+        acc.x += (double)r * (double)r;
+        acc.y += (double)r * (double)z;
+      }
+      s = gsum(acc);
+      rr = s.x;
+      const double rho_next = s.y;
+      if (rr < eps) {
+        conv = true;
+        break;
+      }
+      const float beta = (float)(rho_next / rho);
+      for (int64_t e = gtid; e < nm; e += gthreads) P[e] = fmaf(beta, P[e], AP[e]);
+      rho = rho_next;
+      grid.sync();
+    }
+
+    if constexpr (NODEWISE) {
+      if (out.nodewise) {
+        float* nw = out.nodewise + out.nodewise_off[pid];
+        int64_t i = gtid / m, l = gtid % m;
+        for (int64_t e = gtid; e < nm; e += gthreads) {
+          nw[swap ? l * n + i : e] = X[e];
+          l += dl;
+          i += di;
+          if (l >= m) {
+            l -= m;
+            ++i;
+          }
+        }
+      }
+    }
+    if (gtid == 0) {
+      if (out.value) out.value[pid] = value;
+      if (out.iters) out.iters[pid] = (int32_t)it;
+      if (out.conv) out.conv[pid] = conv ? 1 : 0;
+      if (out.residual) out.residual[pid] = (float)sqrt(rr);
+      if (out.pair_a) out.pair_a[pid] = ga;
+      if (out.pair_b) out.pair_b[pid] = gb;
+      const double kval = conv ? value : __longlong_as_double(0x7ff8000000000000ll);
+      if (out.K) {
+        out.K[(int64_t)ga * out.G + gb] = kval;
+        out.K[(int64_t)gb * out.G + ga] = kval;
+      }
+      if (out.K_iters) {
+        out.K_iters[(int64_t)ga * out.G + gb] = (int32_t)it;
+        out.K_iters[(int64_t)gb * out.G + ga] = (int32_t)it;
+      }
+      if (out.K_conv) {
+        out.K_conv[(int64_t)ga * out.G + gb] = conv;
+        out.K_conv[(int64_t)gb * out.G + ga] = conv;
+      }
+    }
+    grid.sync();
+  }
+}
+
+template <int EK, bool NODEWISE>
+static cudaError_t launch_grid_ek(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,
+                                  const PairJob& job, const SolveParams& prm, const SolveOut& out, float* vec,
+                                  int64_t vstride, double2* gbuf, int nblocks, cudaStream_t stream) {
+  auto kern = k_pcg_grid<EK, NODEWISE>;
+  const size_t smem = kPanelStaticSmem;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  DatasetDev a0 = ds;
+  KernelDesc a1 = vk, a2 = ek;
+  PairJob a3 = job;
+  SolveParams a4 = prm;
+  SolveOut a5 = out;
+  void* args[] = {&a0, &a1, &a2, &a3, &a4, &a5, &vec, &vstride, &gbuf};
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(nblocks), dim3(kPT), args, smem, stream);
+}
+
+int grid_blocks(int num_sms) {
+  int per_sm = 0;
+  cudaFuncSetAttribute(k_pcg_grid<KK_SE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelStaticSmem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_grid<KK_SE, false>, kPT, kPanelStaticSmem) !=
+      cudaSuccess)
+    per_sm = 1;
+  int nw = 0;
+  cudaFuncSetAttribute(k_pcg_grid<KK_SE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelStaticSmem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nw, k_pcg_grid<KK_SE, true>, kPT, kPanelStaticSmem) ==
+          cudaSuccess &&
+      nw < per_sm)
+    per_sm = nw;
+  return (per_sm < 1 ? 1 : per_sm) * num_sms;
+}
+
+template <bool NODEWISE>
+static cudaError_t launch_grid_nw(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,
+                                  const PairJob& job, const SolveParams& prm, const SolveOut& out, float* vec,
+                                  int64_t vstride, double2* gbuf, int nblocks, cudaStream_t stream) {
+  int kind = prm.labeled ? ek.kind : KK_NONE;
+  if (kind == KK_CONST1) kind = KK_NONE;
+  switch (kind) {
+    case KK_SE: return launch_grid_ek<KK_SE, NODEWISE>(ds, vk, ek, job, prm, out, vec, vstride, gbuf, nblocks, stream);
+    case KK_DELTA:
+      return launch_grid_ek<KK_DELTA, NODEWISE>(ds, vk, ek, job, prm, out, vec, vstride, gbuf, nblocks, stream);
+    case KK_POLY:
+      return launch_grid_ek<KK_POLY, NODEWISE>(ds, vk, ek, job, prm, out, vec, vstride, gbuf, nblocks, stream);
+    default:
+      return launch_grid_ek<KK_NONE, NODEWISE>(ds, vk, ek, job, prm, out, vec, vstride, gbuf, nblocks, stream);
+  }
+}
+
+cudaError_t launch_pcg_grid(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
+                            const SolveParams& prm, const SolveOut& out, float* vec, int64_t vstride, double2* gbuf,
+                            int nblocks, cudaStream_t stream) {
+  if (job.npairs < 1) return cudaSuccess;
+  if (out.nodewise)
+    return launch_grid_nw<true>(ds, vk, ek, job, prm, out, vec, vstride, gbuf, nblocks, stream);
+  return launch_grid_nw<false>(ds, vk, ek, job, prm, out, vec, vstride, gbuf, nblocks, stream);
 }
 
 }  // namespace mgk

@@ -185,6 +185,24 @@ def test_panel_nodewise_vs_oracle(mgk):
         assert np.max(np.abs(k.nodewise - o.nodewise)) <= REL * np.max(np.abs(o.nodewise))
 
 
+def test_grid_class_vs_oracle(mgk, monkeypatch):
+    """The whole-device cooperative solver (k_pcg_grid), driven at oracle-sized graphs by
+    lowering its size threshold: Gram (self pairs included) and nodewise pair lists."""
+    from paper_1910_06310_b200 import synth
+
+    monkeypatch.setenv("MGK_GRID_N", "60")
+    rng = np.random.default_rng(12)
+    ds = [synth.protein(rng, int(n)) for n in (70, 130, 180)]
+    _check_gram_vs_oracle(mgk, ds)
+    k = mgk.kernel(ds[0], ds[2], "delta:0.5", "se:1.0")
+    o = O.solve_pcg(ds[0], ds[2], ("delta", 0.5), ("se", 1.0))
+    assert abs(k.value - o.value) <= REL * abs(o.value)
+    assert abs(k.iterations - o.iterations) <= 1
+    assert np.max(np.abs(k.nodewise - o.nodewise)) <= REL * np.max(np.abs(o.nodewise))
+    ul = [mgk.LabeledGraph.from_arrays(g.node_count, g.edges_i, g.edges_j, g.weights, default_q=0.05) for g in ds]
+    _check_gram_vs_oracle(mgk, ul[:2], None, None, tol=1e-6)
+
+
 def test_panel_unlabeled_rgg_vs_oracle(mgk):
     """Config-4 shape (random geometric graphs, unlabeled, tol 1e-6 per SURVEY H1) at reduced n."""
     from paper_1910_06310_b200 import synth

@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -8
+timeout 900 python tools/probe_sizes.py 296 4 1 2>&1 | tail -14
