@@ -1,14 +1,24 @@
-"""Benchmark: all-pairs marginalized-graph-kernel Gram matrix on B200.
+"""Benchmark: all-pairs marginalized-graph-kernel Gram matrices on B200.
 
-Workload (BASELINE.json configs[1]): QM7-shaped synthetic
-molecules, 7165 graphs (n 4..23), Kronecker-delta(0.5) vertex kernel on the
-element label, square-exponential(1.0) edge kernel on the bond length,
-q = 0.05, tol = 1e-10.  One step = the full N(N+1)/2 = 25,672,195-pair Gram
-matrix.  At N GPUs the pair list is sharded (cost-ordered ids round-robin
-over ranks) and the compact per-pair results are gathered to rank 0 (the
-only collective); total work is fixed, so scaling is "strong".
+Default workload (BASELINE.json configs[1]): QM7-shaped
+synthetic molecules, 7165 graphs (n 4..23), Kronecker-delta(0.5) vertex
+kernel on the element label, square-exponential(1.0) edge kernel on the bond
+length, q = 0.05, tol = 1e-10.  One step = the full N(N+1)/2 = 25,672,195-pair
+Gram matrix.  ``--config`` selects the other BASELINE shapes (same JSON line):
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    1    16 random labeled graphs, full 16x16 Gram                (configs[0])
+    2    QM7-shaped, 7165 graphs, all pairs                       (configs[1], default)
+    3    protein-sized, 1000 graphs n 200..600, shuffled + PBR     (configs[2])
+    4    large sparse, 4 density buckets x 25 graphs n 2k..5k,
+         shuffled + PBR, unlabeled, within-bucket Grams (4 x 325) (configs[3])
+    4se  the same with the SE edge kernel (X = 7)
+    5    10k mixed-size molecules (n 4..128), all pairs           (configs[4], values)
+
+At N GPUs the pair list of every Gram is sharded (cost-ordered ids round-robin
+over ranks) and the compact per-pair results are gathered to rank 0 (the only
+collective); total work is fixed, so scaling is "strong".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
 ``--impl reference`` times the CPU oracle port (oracle/mgk_oracle.py, the
 restatement of the reference path; the reference itself is pure Python and
@@ -26,6 +36,7 @@ import subprocess
 import sys
 import threading
 import time
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -34,28 +45,74 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "graph-pairs/sec and effective GFLOP/s vs FP32 peak at 1/2/4/8 B200 vs CPU ref"
-VSPEC, ESPEC, TOL = "delta:0.5", "se:1.0", 1e-10
-X_FLOPS = 7  # 3 + SquareExponential.flop_count (product.py:212-220)
 
 
-def workload(count: int):
+@dataclass
+class Config:
+    key: str
+    text: str
+    vspec: str | None
+    espec: str | None
+    tol: float
+    x_flops: int          # 3 unlabeled, 3 + kappa_e.flop_count labeled (product.py:212-220)
+    reorder: bool         # PBR (seed 0) before the Gram (shuffled inputs)
+    cpu_pairs: int        # default oracle sample for cpu_baseline
+    parity_pairs: int
+    kernel: str           # dominant solver kernel
+
+
+CONFIGS = {
+    "1": Config("1", "config1: 16 random labeled graphs (n 18..22), full 16x16 Gram", "delta:0.5", "se:1.0", 1e-10,
+                7, False, 136, 136, "k_pcg_warp<SE>"),
+    "2": Config("2", "config2: QM7-shaped synthetic molecules, {G} graphs, all-pairs Gram", "delta:0.5", "se:1.0",
+                1e-10, 7, False, 300000, 200, "k_pcg_warp<SE>"),
+    "3": Config("3", "config3: protein-sized synthetic graphs, {G} graphs n 200..600, shuffled + device PBR, "
+                "all-pairs Gram", "delta:0.5", "se:1.0", 1e-10, 7, True, 48, 6, "k_pcg_panel<SE>"),
+    "4": Config("4", "config4: large sparse RGGs, 4 density buckets (mean degree 4/8/16/32) x {B} graphs n 2k..5k, "
+                "shuffled + device PBR, unlabeled, within-bucket Grams", None, None, 1e-6, 3, True, 4, 2,
+                "k_pcg_grid<unlabeled>"),
+    "4se": Config("4se", "config4 with the SE(1.0) edge kernel on the scaled edge length: 4 buckets x {B} graphs",
+                  None, "se:1.0", 1e-10, 7, True, 0, 0, "k_pcg_grid<SE>"),
+    "5": Config("5", "config5: {G} mixed-size synthetic molecules (60% n 4..23, 30% 24..64, 10% 65..128), "
+                "all-pairs Gram", "delta:0.5", "se:1.0", 1e-10, 7, False, 20000, 100, "k_pcg_warp + k_pcg_panel"),
+}
+
+
+def buckets(cfg: Config, count: int | None):
+    """[(name, graphs)] -- one Gram per bucket (config 4: one per density)."""
     from paper_1910_06310_b200 import synth
 
-    return synth.config2(count=count)
+    if cfg.key == "1":
+        return [("all", synth.config1())]
+    if cfg.key == "2":
+        return [("all", synth.config2(count=count or 7165))]
+    if cfg.key == "3":
+        return [("all", synth.config3(count=count or 1000))]
+    if cfg.key == "5":
+        return [("all", synth.config5(count=count or 10000))]
+    per = count or 25
+    out = []
+    for k, d in enumerate((4, 8, 16, 32)):
+        gs = synth.config4(count=per, seed=100 + k, degrees=(d,))
+        out.append((f"deg{d}", gs))
+    return out
 
 
-def describe(ds, count):
+def describe(cfg: Config, bks, pairs):
+    graphs = [g for _, b in bks for g in b]
     return {
-        "workload": f"config2: QM7-shaped synthetic molecules, {count} graphs, all-pairs Gram",
-        "graphs": count,
-        "pairs": count * (count + 1) // 2,
-        "nodes_mean": float(np.mean([g.node_count for g in ds])),
-        "edges_mean": float(np.mean([g.edge_count for g in ds])),
-        "vertex_kernel": VSPEC,
-        "edge_kernel": ESPEC,
+        "workload": cfg.text.format(G=len(graphs), B=len(bks[0][1])),
+        "graphs": len(graphs),
+        "pairs": pairs,
+        "nodes_mean": float(np.mean([g.node_count for g in graphs])),
+        "edges_mean": float(np.mean([g.edge_count for g in graphs])),
+        "vertex_kernel": cfg.vspec,
+        "edge_kernel": cfg.espec,
         "q": 0.05,
-        "tol": TOL,
-        "cache": "L2 flushed (256 MiB device write) before every timed step; inputs are smaller than L2",
+        "tol": cfg.tol,
+        "reorder": "pbr seed 0 (device)" if cfg.reorder else "none",
+        "cache": "L2 flushed (256 MiB device write) before every timed step; the dataset is smaller than L2, the "
+                 "solver state of configs 3-4 is not",
     }
 
 
@@ -63,35 +120,54 @@ def describe(ds, count):
 # CPU oracle leg (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
 
-_POOL_DS = None
+_POOL = {}
 
 
-def _oracle_pair(ab):
+def _oracle_pair(job):
     from oracle import mgk_oracle as O
 
-    a, b = ab
-    r = O.solve_pcg(_POOL_DS[a], _POOL_DS[b], ("delta", 0.5), ("se", 1.0), tol=TOL)
+    b, x, y = job
+    ds, vspec, espec, tol = _POOL["ds"][b], _POOL["v"], _POOL["e"], _POOL["tol"]
+    if espec is None:
+        system = O.FactoredSystem(ds[x], ds[y], vspec)
+        r = O.solve_pcg(ds[x], ds[y], vspec, None, tol=tol, system=system)
+    else:
+        r = O.solve_pcg(ds[x], ds[y], vspec, espec, tol=tol)
     return r.value, r.iterations
 
 
-def cpu_pairs_per_sec(ds, npairs: int, seed: int, procs: int):
+def _spec(s):
+    from oracle import mgk_oracle as O
+
+    return O.parse_spec(s) if s else None
+
+
+def sample_pairs(bks, npairs: int, seed: int):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(npairs):
+        b = int(rng.integers(0, len(bks)))
+        G = len(bks[b][1])
+        x, y = sorted(rng.integers(0, G, size=2).tolist())
+        out.append((b, x, y))
+    return out
+
+
+def cpu_pairs_per_sec(cfg: Config, bks, npairs: int, seed: int, procs: int):
     """Time the oracle (float64 numpy restatement of solve_pcg) on a random pair sample."""
     import multiprocessing as mp
 
-    global _POOL_DS
-    _POOL_DS = ds
-    rng = np.random.default_rng(seed)
-    G = len(ds)
-    a = rng.integers(0, G, size=npairs)
-    b = rng.integers(0, G, size=npairs)
-    pairs = [(int(min(x, y)), int(max(x, y))) for x, y in zip(a, b)]
+    _POOL.update(ds=[b for _, b in bks], v=_spec(cfg.vspec), e=_spec(cfg.espec), tol=cfg.tol)
+    jobs = sample_pairs(bks, npairs, seed)
     ctx = mp.get_context("fork")
+    procs = max(1, min(procs, npairs))
     with ctx.Pool(procs) as pool:
-        pool.map(_oracle_pair, pairs[: procs * 2], chunksize=1)  # warm the workers
+        if npairs >= 4 * procs:
+            pool.map(_oracle_pair, jobs[: procs], chunksize=1)  # warm the workers
         t0 = time.perf_counter()
-        out = pool.map(_oracle_pair, pairs, chunksize=max(1, npairs // (procs * 8)))
+        out = pool.map(_oracle_pair, jobs, chunksize=max(1, npairs // (procs * 8)))
         dt = time.perf_counter() - t0
-    return npairs / dt, dt, pairs, out
+    return npairs / dt, dt, jobs, out
 
 
 # ---------------------------------------------------------------------------
@@ -159,9 +235,9 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def traffic_from_profiles():
-    """dram bytes per launch of the solver kernel from the committed ncu capture, if any."""
-    for p in sorted((ROOT / "profiles").glob("*ncu_summary*.json"), reverse=True):
+def traffic_from_profiles(cfg: Config):
+    """dram bytes per launch of the solver kernel from the committed ncu capture of this config, if any."""
+    for p in sorted((ROOT / "profiles").glob(f"*ncu_summary_c{cfg.key}*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
             return d.get("solver_dram_bytes_per_launch"), p.name
@@ -170,12 +246,21 @@ def traffic_from_profiles():
     return None, None
 
 
+def reorder_dataset(ds, device: int):
+    """Device PBR (seed 0) of every graph, applied on the host (the public API path)."""
+    from paper_1910_06310_b200 import apply_permutation, pbr_reorder_many
+
+    perms = pbr_reorder_many(ds, seed=0, device=device)
+    return [apply_permutation(g, p) for g, p in zip(ds, perms)]
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
     from paper_1910_06310_b200 import native
     from paper_1910_06310_b200.gram import compute_gram
 
+    cfg = CONFIGS[args.config]
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -183,12 +268,17 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
-    ds = workload(args.count)
-    G = len(ds)
-    ctx = native.Context(local_rank)
-    pk = native.PackedDataset(ds)
-    ctx.upload(pk)
-    ctx.set_kernels(VSPEC, ESPEC)
+    raw = buckets(cfg, args.count)
+    t_pre = time.perf_counter()
+    bks = [(name, reorder_dataset(ds, local_rank) if cfg.reorder else ds) for name, ds in raw]
+    reorder_s = time.perf_counter() - t_pre
+    ctxs = []
+    for _, ds in bks:
+        ctx = native.Context(local_rank)
+        ctx.upload(native.PackedDataset(ds))
+        ctx.set_kernels(cfg.vspec, cfg.espec)
+        ctxs.append(ctx)
+    npairs = sum(len(ds) * (len(ds) + 1) // 2 for _, ds in bks)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
     def barrier():
@@ -197,33 +287,40 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     def step():
-        """One Gram (N=1: device-resident result; N>1: shard + gather to rank 0)."""
-        if world == 1:
-            ctx.gram(TOL, fetch=False)
+        """One Gram per bucket (N=1: device-resident result; N>1: shard + gather to rank 0)."""
+        ms_tot, nl_tot, g_tot = 0.0, 0, 0.0
+        for ctx, (_, ds) in zip(ctxs, bks):
+            if world == 1:
+                ctx.gram(cfg.tol, fetch=False)
+                ms, launches = ctx.last_timing()
+                ms_tot += ms
+                nl_tot += launches
+                continue
+            pa, pb, v, it, cv = ctx.gram_shard(rank, world, cfg.tol)
             ms, launches = ctx.last_timing()
-            return ms, launches, 0.0
-        pa, pb, v, it, cv = ctx.gram_shard(rank, world, TOL)
-        ms, launches = ctx.last_timing()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
-        payload = torch.from_numpy(np.stack([pa.astype(np.float64), pb.astype(np.float64), v,
-                                             it.astype(np.float64) + 0.5 * cv]).T.copy()).to(dev)
-        n = torch.tensor([payload.shape[0]], device=dev)
-        nmax = n.clone()
-        dist.all_reduce(nmax, op=dist.ReduceOp.MAX)
-        pad = torch.zeros((int(nmax.item()), 4), dtype=torch.float64, device=dev)
-        pad[: payload.shape[0]] = payload
-        pad[payload.shape[0]:, 0] = -1
-        out = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
-        dist.gather(pad, out, dst=0)
-        t1.record()
-        torch.cuda.synchronize(dev)
-        if rank == 0:
-            allp = torch.cat(out).cpu().numpy()
-            allp = allp[allp[:, 0] >= 0]
-            assemble(allp, G)
-        return ms, launches, t0.elapsed_time(t1)
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            payload = torch.from_numpy(np.stack([pa.astype(np.float64), pb.astype(np.float64), v,
+                                                 it.astype(np.float64) + 0.5 * cv]).T.copy()).to(dev)
+            n = torch.tensor([payload.shape[0]], device=dev)
+            nmax = n.clone()
+            dist.all_reduce(nmax, op=dist.ReduceOp.MAX)
+            pad = torch.zeros((int(nmax.item()), 4), dtype=torch.float64, device=dev)
+            pad[: payload.shape[0]] = payload
+            pad[payload.shape[0]:, 0] = -1
+            out = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
+            dist.gather(pad, out, dst=0)
+            t1.record()
+            torch.cuda.synchronize(dev)
+            if rank == 0:
+                allp = torch.cat(out).cpu().numpy()
+                allp = allp[allp[:, 0] >= 0]
+                assemble(allp, len(ds))
+            ms_tot += ms
+            nl_tot += launches
+            g_tot += t0.elapsed_time(t1)
+        return ms_tot, nl_tot, g_tot
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -245,50 +342,73 @@ def run_ours(args, rank, world, local_rank):
     if dist is not None:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step, ms_solve = float(t_local[0]), float(t_local[1])
-    npairs = G * (G + 1) // 2
     value = npairs / (ms_step * 1e-3)
 
     result = None
     if rank == 0:
-        # ---- parity spot check + algorithmic flops from the iteration counts (outside the timed region)
-        K, it, cv = ctx.gram(TOL) if world == 1 else ctx.gram(TOL)
-        n = np.array([g.node_count for g in ds], dtype=np.float64)
-        S = 2.0 * np.array([g.edge_count for g in ds], dtype=np.float64)
-        iu, ju = np.triu_indices(G)
-        iters = it[iu, ju].astype(np.float64)
-        flops = float(np.sum(iters * (X_FLOPS * S[iu] * S[ju] + 15.0 * n[iu] * n[ju])))
-        exps = float(np.sum(iters * S[iu] * S[ju]))
-        del iu, ju
+        # ---- parity sample + algorithmic flops from the iteration counts (outside the timed region)
         from oracle import mgk_oracle as O
 
-        rng = np.random.default_rng(1)
-        worst, it_dev = 0.0, 0
-        for _ in range(200):
-            a, b = sorted(rng.integers(0, G, size=2).tolist())
-            o = O.solve_pcg(ds[a], ds[b], ("delta", 0.5), ("se", 1.0), tol=TOL)
-            worst = max(worst, abs(K[a, b] - o.value) / abs(o.value))
-            it_dev = max(it_dev, abs(int(it[a, b]) - o.iterations))
-        fp32_peak, ex2_peak = ctx.peaks(local_rank)
-        achieved = flops / (ms_solve * 1e-3) / 1e12 * (1 if world == 1 else 1.0 / world)
-        traffic, traffic_src = traffic_from_profiles()
+        flops = exps = 0.0
+        Ks = []
+        for ctx, (_, ds) in zip(ctxs, bks):
+            K, it, cv = ctx.gram(cfg.tol)
+            Ks.append((K, it))
+            G = len(ds)
+            n = np.array([g.node_count for g in ds], dtype=np.float64)
+            S = 2.0 * np.array([g.edge_count for g in ds], dtype=np.float64)
+            iu, ju = np.triu_indices(G)
+            iters = it[iu, ju].astype(np.float64)
+            flops += float(np.sum(iters * (cfg.x_flops * S[iu] * S[ju] + 15.0 * n[iu] * n[ju])))
+            exps += float(np.sum(iters * S[iu] * S[ju])) if cfg.espec == "se:1.0" else 0.0
+            del iu, ju
+        worst, it_dev, checked = 0.0, 0, 0
+        if cfg.parity_pairs:
+            vs, es = _spec(cfg.vspec), _spec(cfg.espec)
+            for b, x, y in sample_pairs(bks, cfg.parity_pairs, 1):
+                ds = bks[b][1]
+                system = O.FactoredSystem(ds[x], ds[y], vs) if es is None else None
+                o = O.solve_pcg(ds[x], ds[y], vs, es, tol=cfg.tol, system=system)
+                K, it = Ks[b]
+                worst = max(worst, abs(K[x, y] - o.value) / abs(o.value))
+                it_dev = max(it_dev, abs(int(it[x, y]) - o.iterations))
+                checked += 1
+        del Ks
+        fp32_peak, ex2_peak = ctxs[0].peaks(local_rank)
+        achieved = flops / world / (ms_solve * 1e-3) / 1e12
+        traffic, traffic_src = traffic_from_profiles(cfg)
 
-        # ---- end to end through the public API with host buffers (N=1 leg; rank 0 shard at N>1)
+        # ---- end to end through the public API with host buffers (rank 0)
         e2e_ms = []
-        h0, d0 = ctx.transfer_bytes()
+        h0, d0 = ctxs[0].transfer_bytes()
         nrep = max(1, min(args.steps, 3))
         for _ in range(nrep):
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            res = compute_gram(ds, VSPEC, ESPEC, device=local_rank)
+            for _, ds in raw:
+                src = reorder_dataset(ds, local_rank) if cfg.reorder else ds
+                res = compute_gram(src, cfg.vspec, cfg.espec, cfg=_solver_cfg(cfg), device=local_rank)
+                assert res.matrix.shape == (len(ds), len(ds))
             torch.cuda.synchronize(dev)
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        h1, d1 = ctx.transfer_bytes()
-        assert res.matrix.shape == (G, G)
+        h1, d1 = ctxs[0].transfer_bytes()
         e2e_val = npairs / (float(np.mean(e2e_ms)) * 1e-3)
 
         # ---- CPU oracle baseline on this host
         cores = os.cpu_count() or 1
-        cpu_rate, cpu_dt, _, _ = cpu_pairs_per_sec(ds, args.cpu_pairs, 7, cores)
+        cpu = None
+        ncpu = args.cpu_pairs if args.cpu_pairs is not None else cfg.cpu_pairs
+        if ncpu:
+            cpu_rate, cpu_dt, _, _ = cpu_pairs_per_sec(cfg, bks, ncpu, 7, cores)
+            cpu = {
+                "value": cpu_rate,
+                "unit": "pairs/s",
+                "cores": min(cores, ncpu),
+                "kind": "port",
+                "sample": f"{ncpu} uniformly sampled pairs of this workload, oracle/mgk_oracle.solve_pcg (float64 "
+                          f"numpy{', factored unlabeled system' if cfg.espec is None else ''}), multiprocessing "
+                          f"pool of {min(cores, ncpu)} processes, {cpu_dt:.1f} s",
+            }
 
         result = {
             "metric": METRIC,
@@ -302,8 +422,8 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f32",
-            "data": "synthetic (seeded QM7-shaped generator, paper_1910_06310_b200/synth.py)",
-            "config": describe(ds, G),
+            "data": "synthetic (seeded generators, paper_1910_06310_b200/synth.py)",
+            "config": describe(cfg, bks, npairs),
             "effective_gflops": flops / (ms_step * 1e-3) / 1e9,
             "roofline": {
                 "bound": "fp32",
@@ -315,22 +435,15 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": "FFMA microbenchmark measured live in this run (mgk_bench_peaks); "
                                "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
                 "flops_per_launch": flops / world,
-                "flops_convention": "sum over pairs of I*(X*S_a*S_b + 15*n_a*n_b), X=7 (SURVEY §8d)",
+                "flops_convention": f"sum over pairs of I*(X*S_a*S_b + 15*n_a*n_b), X={cfg.x_flops} (SURVEY §8d)",
                 "ex2_per_launch": exps / world,
                 "ex2_achieved_tops": exps / world / (ms_solve * 1e-3) / 1e12,
                 "ex2_peak_tops": ex2_peak,
                 "ex2_frac": exps / world / (ms_solve * 1e-3) / 1e12 / ex2_peak,
-                "kernel": "k_pcg_warp<24,10,SE>",
+                "kernel": cfg.kernel,
                 "traffic_source": traffic_src,
             },
-            "cpu_baseline": {
-                "value": cpu_rate,
-                "unit": "pairs/s",
-                "cores": cores,
-                "kind": "port",
-                "sample": f"{args.cpu_pairs} uniformly sampled config2 pairs, oracle/mgk_oracle.solve_pcg (float64 "
-                          f"numpy), multiprocessing pool of {cores} processes, {cpu_dt:.1f} s",
-            },
+            "cpu_baseline": cpu,
             "e2e": {
                 "value": e2e_val,
                 "unit": "pairs/s",
@@ -338,18 +451,27 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": (d1 - d0) // nrep,
                 "ms_per_step": float(np.mean(e2e_ms)),
                 "api": "paper_1910_06310_b200.compute_gram (validate, pack, C-ABI upload, device octiles, solve, "
-                       "D2H of the N x N matrix, iterations and flags)",
+                       "D2H of the N x N matrix, iterations and flags)"
+                       + (" after pbr_reorder_many + apply_permutation" if cfg.reorder else ""),
             },
             "gpu_launches": launches,
             "clocks": clocks.summary(),
-            "parity": {"sample_pairs": 200, "max_rel_err": worst, "max_iter_diff": it_dev,
+            "parity": {"sample_pairs": checked, "max_rel_err": worst, "max_iter_diff": it_dev,
                        "bar": "1e-5 relative, +-1 iteration"},
             "solve_ms_per_step": ms_solve,
         }
+        if cfg.reorder:
+            result["preprocess_s"] = {"device_pbr_and_apply": reorder_s}
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def _solver_cfg(cfg: Config):
+    from paper_1910_06310_b200 import SolverConfig
+
+    return SolverConfig(tolerance=cfg.tol)
 
 
 def assemble(rows: np.ndarray, G: int):
@@ -372,19 +494,24 @@ def assemble(rows: np.ndarray, G: int):
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    ds = workload(args.count)
+    cfg = CONFIGS[args.config]
+    bks = buckets(cfg, args.count)
+    npairs = sum(len(ds) * (len(ds) + 1) // 2 for _, ds in bks)
+    if not cfg.cpu_pairs:
+        return {"impl": "reference", "unavailable": f"config {cfg.key}: the labeled product systems are too large "
+                "for the float64 oracle (S_a*S_b up to 1e10 nonzeros)"}
     cores = os.cpu_count() or 1
-    per_step = args.ref_pairs
+    per_step = args.ref_pairs if args.ref_pairs is not None else max(cfg.cpu_pairs // 3, cores)
     for w in range(args.warmup):
-        cpu_pairs_per_sec(ds, max(cores * 4, per_step // 8), 100 + w, cores)
+        cpu_pairs_per_sec(cfg, bks, max(cores, per_step // 8), 100 + w, cores)
     rates, times = [], []
     for k in range(args.steps):
-        r, dt, _, _ = cpu_pairs_per_sec(ds, per_step, 1000 + k, cores)
+        r, dt, _, _ = cpu_pairs_per_sec(cfg, bks, per_step, 1000 + k, cores)
         rates.append(r)
         times.append(dt)
     value = per_step * len(times) / sum(times)
-    sample = (f"{per_step} uniformly sampled config2 pairs per step, oracle/mgk_oracle.solve_pcg (float64 numpy "
-              f"restatement of the reference solve_pcg), {cores} processes")
+    sample = (f"{per_step} uniformly sampled pairs of this workload per step, oracle/mgk_oracle.solve_pcg (float64 "
+              f"numpy restatement of the reference solve_pcg), {min(cores, per_step)} processes")
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -398,9 +525,10 @@ def run_reference(args, rank, world):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded QM7-shaped generator)",
-        "config": describe(ds, len(ds)),
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": "port", "sample": sample},
+        "data": "synthetic (seeded generators)",
+        "config": describe(cfg, bks, npairs),
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": min(cores, per_step), "kind": "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -411,9 +539,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--count", type=int, default=7165)
-    ap.add_argument("--cpu-pairs", type=int, default=300000)
-    ap.add_argument("--ref-pairs", type=int, default=100000)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
+    ap.add_argument("--count", type=int, default=None, help="graphs (per bucket for config 4)")
+    ap.add_argument("--cpu-pairs", type=int, default=None)
+    ap.add_argument("--ref-pairs", type=int, default=None)
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
