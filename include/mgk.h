@@ -102,6 +102,24 @@ int mgk_gram_shard(mgk_ctx* ctx, int rank, int world, double tol, int64_t max_it
 int mgk_pairs(mgk_ctx* ctx, int64_t npairs, const int32_t* a, const int32_t* b, double tol, int64_t max_iter,
               double* value, int32_t* iters, double* residual, uint8_t* conv, double* nodewise);
 
+/* Consumer of streamed nodewise results: one call per chunk of solved pairs.
+ * offsets[k] .. offsets[k+1] index pair k's n_a x n_b float32 field inside
+ * `nodewise` (row-major, first graph's nodes as rows).  Buffers are valid only
+ * during the call.  Return 0 to continue, nonzero to abort the stream. */
+typedef int (*mgk_nodewise_sink)(void* user, int64_t npairs, const int32_t* a, const int32_t* b, const double* value,
+                                 const int32_t* iters, const uint8_t* conv, const int64_t* offsets,
+                                 const float* nodewise);
+
+/* Nodal similarity of every Gram pair (a <= b) of this rank's shard (pair ids
+ * congruent to rank modulo world, as mgk_gram_shard), streamed to `sink` in
+ * chunks of at most chunk_bytes of float32 field (the per-pair KernelResult.
+ * nodewise of solver.py:212-246 for all N(N+1)/2 pairs of gram.py:57-95; the
+ * full field of a 10k-graph dataset exceeds device memory, so it is produced
+ * and handed off chunk by chunk through pinned host buffers).  Reports the
+ * pairs and floats streamed. */
+int mgk_gram_nodewise(mgk_ctx* ctx, int rank, int world, double tol, int64_t max_iter, int64_t chunk_bytes,
+                      mgk_nodewise_sink sink, void* user, int64_t* npairs_out, int64_t* nfloats_out);
+
 /* Single pair convenience wrapper of mgk_pairs (mgkbind.kernel, __init__.py:41-67). */
 int mgk_kernel(mgk_ctx* ctx, int32_t a, int32_t b, double tol, int64_t max_iter, double* value, double* nodewise,
                int32_t* iters, double* residual, uint8_t* conv);

@@ -223,6 +223,12 @@ struct mgk_ctx {
   DBuf<int64_t> d_nwoff;
   DBuf<int32_t> d_pa, d_pb, d_rowcol;
   DBuf<int64_t> d_rowpre;
+  // host images of the Gram job lists (host-side pair decoding for streaming)
+  std::vector<int32_t> h_lists, h_rowcol;
+  std::vector<int64_t> h_rowpre;
+  // pinned staging for streamed nodewise chunks
+  float* h_nw = nullptr;
+  size_t h_nw_cap = 0;
 };
 
 extern "C" {
@@ -256,6 +262,7 @@ int mgk_ctx_destroy(mgk_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
+  if (ctx->h_nw) cudaFreeHost(ctx->h_nw);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return MGK_OK;
@@ -637,7 +644,7 @@ static bool panel_dataset(const mgk_ctx* c) {
   if (c->ds.el_dim > 1) return false;
   if (getenv("MGK_NO_PANEL")) return false;
   for (const GraphDesc& d : c->graphs)
-    if (2 * d.ne > 128 && d.npanels <= 0) return false;
+    if (d.npanels <= 0) return false;
   return true;
 }
 
@@ -679,8 +686,12 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     } else if (j.kernel == JK_PANEL) {
       const int64_t nm = j.max_n * j.max_m;
       slabs[k] = 5 * ((nm + 31) / 32 * 32);
-      svec[k] = (int)(2 * std::min<int64_t>(nm, kPanelSmemNM));
-      ctas[k] = panel_ctas_per_sm(svec[k]) * c->num_sms;
+      // P and Ap in shared memory when every pair of the job fits; else all pairs keep them in HBM/L2
+      // and the whole L1 stays available to the gathers
+      svec[k] = nm <= kPanelSmemNM ? (int)(2 * nm) : 0;
+      int per_sm = panel_ctas_per_sm(svec[k]);
+      if (const char* e = getenv("MGK_PANEL_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
+      ctas[k] = per_sm * c->num_sms;
     } else {
       continue;
     }
@@ -790,6 +801,9 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   col.insert(col.end(), tcol.begin(), tcol.end());
   CUDA_TRY(c->d_rowpre.upload(pre, s));
   CUDA_TRY(c->d_rowcol.upload(col, s));
+  c->h_lists = lists;
+  c->h_rowpre = pre;
+  c->h_rowcol = col;
   const int32_t* dsmall = c->d_list_a.ptr;
   const int32_t* dmid = dsmall + ns;
   const int32_t* dlarge = dmid + nmid;
@@ -903,6 +917,116 @@ int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter
   if (value) CUDA_TRY(d2h(value, c->d_value.ptr, total * sizeof(double)));
   if (iters) CUDA_TRY(d2h(iters, c->d_iters.ptr, total * sizeof(int32_t)));
   if (conv) CUDA_TRY(d2h(conv, c->d_conv.ptr, total));
+  return MGK_OK;
+}
+
+// Host image of a Gram job (device list pointers rebased onto the host copies).
+static PairJob host_job(const mgk_ctx* c, const PairJob& j) {
+  PairJob h = j;
+  auto rebase32 = [&](const int32_t* p, const DBuf<int32_t>& d, const std::vector<int32_t>& hv) -> const int32_t* {
+    return p ? hv.data() + (p - d.ptr) : nullptr;
+  };
+  h.list_a = rebase32(j.list_a, c->d_list_a, c->h_lists);
+  h.list_b = rebase32(j.list_b, c->d_list_a, c->h_lists);
+  h.row_col0 = rebase32(j.row_col0, c->d_rowcol, c->h_rowcol);
+  h.row_prefix = j.row_prefix ? c->h_rowpre.data() + (j.row_prefix - c->d_rowpre.ptr) : nullptr;
+  return h;
+}
+
+int mgk_gram_nodewise(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter, int64_t chunk_bytes,
+                      mgk_nodewise_sink sink, void* user, int64_t* npairs_out, int64_t* nfloats_out) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (world < 1 || rank < 0 || rank >= world) return fail(MGK_E_INVALID, "bad rank/world");
+  if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
+  if (!sink) return fail(MGK_E_INVALID, "null sink");
+  int rc = prepare(c);
+  if (rc) return rc;
+  std::vector<JobSpec> jobs;
+  rc = gram_jobs(c, jobs);
+  if (rc) return rc;
+  const SolveParams prm = make_params(c, tol, max_iter);
+  int64_t max_pair = 0;
+  for (const GraphDesc& d : c->graphs) max_pair = std::max<int64_t>(max_pair, d.n);
+  max_pair *= max_pair;
+  const int64_t cap = std::max<int64_t>(chunk_bytes / 4, max_pair);
+  const int64_t pair_cap = 1 << 22;
+  if (c->h_nw_cap < (size_t)cap) {
+    if (c->h_nw) cudaFreeHost(c->h_nw);
+    c->h_nw = nullptr;
+    c->h_nw_cap = 0;
+    CUDA_TRY(cudaMallocHost(&c->h_nw, (size_t)cap * sizeof(float)));
+    c->h_nw_cap = (size_t)cap;
+  }
+  CUDA_TRY(c->d_nodewise.alloc(cap));
+  CUDA_TRY(c->d_value.alloc(pair_cap));
+  CUDA_TRY(c->d_iters.alloc(pair_cap));
+  CUDA_TRY(c->d_conv.alloc(pair_cap));
+  CUDA_TRY(c->d_pa.alloc(pair_cap));
+  CUDA_TRY(c->d_pb.alloc(pair_cap));
+  std::vector<int64_t> offs;
+  std::vector<int32_t> ha, hb, hi;
+  std::vector<double> hv;
+  std::vector<uint8_t> hc;
+  int64_t total_pairs = 0, total_floats = 0;
+  double ms_total = 0.0;
+  int launches = 0;
+  for (const JobSpec& js : jobs) {
+    if (js.job.npairs <= 0) continue;
+    const PairJob hj = host_job(c, js.job);
+    const int64_t local = shard_len(js.job.npairs, rank, world);
+    for (int64_t q0 = 0; q0 < local;) {
+      // chunk [q0, q1): field floats <= cap and pairs <= pair_cap
+      offs.assign(1, 0);
+      int64_t q1 = q0;
+      while (q1 < local && q1 - q0 < pair_cap) {
+        int32_t a, b;
+        decode_pair(hj, rank + q1 * (int64_t)world, a, b);
+        const int64_t f = (int64_t)c->graphs[a].n * c->graphs[b].n;
+        if (offs.back() + f > cap) break;
+        offs.push_back(offs.back() + f);
+        ++q1;
+      }
+      const int64_t np = q1 - q0;
+      CUDA_TRY(c->d_nwoff.upload(offs, c->stream));
+      JobSpec chunk = js;
+      chunk.job.offset = rank + q0 * (int64_t)world;
+      chunk.job.stride = world;
+      chunk.job.npairs = np;
+      std::vector<JobSpec> one = {chunk};
+      SolveOut o{};
+      o.value = c->d_value.ptr;
+      o.iters = c->d_iters.ptr;
+      o.conv = c->d_conv.ptr;
+      o.pair_a = c->d_pa.ptr;
+      o.pair_b = c->d_pb.ptr;
+      o.nodewise = c->d_nodewise.ptr;
+      o.nodewise_off = c->d_nwoff.ptr;
+      rc = run_jobs(c, one, o, {0}, prm);
+      if (rc) return rc;
+      ms_total += c->last_ms;
+      launches += c->last_launches;
+      ha.resize(np);
+      hb.resize(np);
+      hi.resize(np);
+      hv.resize(np);
+      hc.resize(np);
+      CUDA_TRY(d2h(ha.data(), c->d_pa.ptr, np * sizeof(int32_t)));
+      CUDA_TRY(d2h(hb.data(), c->d_pb.ptr, np * sizeof(int32_t)));
+      CUDA_TRY(d2h(hv.data(), c->d_value.ptr, np * sizeof(double)));
+      CUDA_TRY(d2h(hi.data(), c->d_iters.ptr, np * sizeof(int32_t)));
+      CUDA_TRY(d2h(hc.data(), c->d_conv.ptr, np));
+      CUDA_TRY(d2h(c->h_nw, c->d_nodewise.ptr, offs.back() * sizeof(float)));
+      if (sink(user, np, ha.data(), hb.data(), hv.data(), hi.data(), hc.data(), offs.data(), c->h_nw) != 0)
+        return fail(MGK_E_STATE, "nodewise sink aborted the stream");
+      total_pairs += np;
+      total_floats += offs.back();
+      q0 = q1;
+    }
+  }
+  c->last_ms = ms_total;
+  c->last_launches = launches;
+  if (npairs_out) *npairs_out = total_pairs;
+  if (nfloats_out) *nfloats_out = total_floats;
   return MGK_OK;
 }
 

@@ -53,8 +53,11 @@ struct GraphDesc {
   int32_t pad;
 };
 
-// Row panels (pcg_panel.cu): consecutive rows whose nonzeros fit 32 lanes x 8 slots.
-constexpr int kPanelSlots = 8;
+// Row panels (pcg_panel.cu): consecutive rows whose nonzeros fit 32 lanes x kPanelSlots.
+#ifndef MGK_PANEL_SLOTS
+#define MGK_PANEL_SLOTS 8
+#endif
+constexpr int kPanelSlots = MGK_PANEL_SLOTS;
 constexpr int kPanelCap = 32 * kPanelSlots;
 
 // Base-kernel descriptor (basekernels.py:60-172); kind codes match basekernels.py.

@@ -52,12 +52,26 @@ struct SolveParams {
   int32_t tiny_nm;          // n*m at or below which the warp solver runs the pair in FP64
 };
 
+// Gram modes report a <= b (the reference's pair order, gram.py:38-54); lists keep the caller's order.
+__host__ __device__ inline void decode_gram_pair(const PairJob& j, int64_t pid, int32_t& a, int32_t& b);
+
 __host__ __device__ inline void decode_pair(const PairJob& j, int64_t q, int32_t& a, int32_t& b) {
   const int64_t pid = j.offset + q * j.stride;
   if (j.mode == PM_LIST) {
     a = j.list_a[pid];
     b = j.list_b[pid];
-  } else if (j.mode == PM_RAGGED) {
+    return;
+  }
+  decode_gram_pair(j, pid, a, b);
+  if (a > b) {
+    const int32_t t = a;
+    a = b;
+    b = t;
+  }
+}
+
+__host__ __device__ inline void decode_gram_pair(const PairJob& j, int64_t pid, int32_t& a, int32_t& b) {
+  if (j.mode == PM_RAGGED) {
     int lo = 0, hi = j.na;  // largest u with row_prefix[u] <= pid
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;

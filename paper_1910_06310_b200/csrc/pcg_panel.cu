@@ -7,7 +7,7 @@
 // Same on-the-fly XMV as pcg_warp.cu, generalised from "the whole lane graph in
 // one warp's registers" to row panels: the lane graph L is cut (once per
 // dataset, on the host from the degree sequence) into panels of consecutive
-// rows holding at most 256 nonzeros; a warp holds one panel in registers
+// rows holding at most 128 nonzeros; a warp holds one panel in registers
 // (lane l owns panel nonzeros l + 32 t, t < NS) and walks a chunk of U rows:
 //
 //   acc[t]  = sum_{k in U(i)} kappa(e_k, e'_t) w_k P[j_k][col_L(t)]
@@ -16,7 +16,7 @@
 //
 // Every (panel, U-row chunk) item writes a disjoint block of AP, so there are
 // no atomics and the result is independent of the warp schedule.  Small lane
-// graphs (S_L <= 64 / 128) use a single panel with 2 / 4 slots per lane.
+// graphs (S_L <= 64) use a single panel with 2 slots per lane.
 //
 // PCG state: P and AP live in shared memory when 2 n m floats fit the per-CTA
 // budget chosen at launch (mid-size pairs), otherwise in a per-CTA slab in HBM
@@ -55,6 +55,66 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
   return s;
 }
 
+#ifndef MGK_PANEL_PIPELINE
+#define MGK_PANEL_PIPELINE 0
+#endif
+#if MGK_PANEL_PIPELINE
+// acc[t] += sum_{k in [k0, k1)} kappa(e_k, e'_t) w_k P[j_k][lcol[t]]   (U row, warp-uniform)
+//
+// P lives in L1/L2 (or shared memory), so the gathers are latency-bound: the
+// loop is software-pipelined over batches of two U nonzeros -- row entries two
+// batches ahead, gathers one batch ahead -- so each warp keeps 2 x NS gathers
+// in flight while it evaluates the edge kernel of the current batch.  Padding
+// entries have weight 0 and point at row 0 (a valid address).
+template <int NS, int EK>
+__device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float4* __restrict__ ue, int k0, int k1,
+                                               const float* P, int m, const int (&lcol)[NS],
+                                               const float (&llab)[NS], float (&acc)[NS]) {
+  if (k0 >= k1) return;
+  auto entry = [&](int k) {
+    return k < k1 ? ue[k] : make_float4(__int_as_float(0), 0.0f, 0.0f, 0.0f);
+  };
+  float4 e0 = entry(k0), e1 = entry(k0 + 1);
+  float4 f0 = entry(k0 + 2), f1 = entry(k0 + 3);
+  float p0[NS], p1[NS];
+  {
+    const float* r0 = P + __float_as_int(e0.x) * m;
+    const float* r1 = P + __float_as_int(e1.x) * m;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      p0[t] = r0[lcol[t]];
+      p1[t] = r1[lcol[t]];
+    }
+  }
+  for (int k = k0; k < k1; k += 2) {
+    // issue the next batch's gathers and the entries of the batch after it
+    const float* s0 = P + __float_as_int(f0.x) * m;
+    const float* s1 = P + __float_as_int(f1.x) * m;
+    float q0[NS], q1[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      q0[t] = s0[lcol[t]];
+      q1[t] = s1[lcol[t]];
+    }
+    const float4 g0 = entry(k + 4), g1 = entry(k + 5);
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      acc[t] = fmaf(edge_kappa<EK>(ek, e0.z, llab[t]), e0.y * p0[t], acc[t]);
+      acc[t] = fmaf(edge_kappa<EK>(ek, e1.z, llab[t]), e1.y * p1[t], acc[t]);
+    }
+    e0 = f0;
+    e1 = f1;
+    f0 = g0;
+    f1 = g1;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      p0[t] = q0[t];
+      p1[t] = q1[t];
+    }
+  }
+}
+
+#else
 // acc[t] += sum_{k in [k0, k1)} kappa(e_k, e'_t) w_k P[j_k][lcol[t]]   (U row, warp-uniform)
 template <int NS, int EK>
 __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float4* __restrict__ ue, int k0, int k1,
@@ -84,6 +144,8 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
     for (int t = 0; t < NS; ++t) acc[t] = fmaf(edge_kappa<EK>(ek, e0.z, llab[t]), e0.y * r0[lcol[t]], acc[t]);
   }
 }
+
+#endif
 
 struct PairView {
   const int32_t* urp;   // U row pointers (relative to ue)
@@ -214,7 +276,7 @@ __device__ __forceinline__ void xmv_dispatch(int ns, const KernelDesc& ek, const
   switch (ns) {
     case 2: xmv_panels<2, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
     case 4: xmv_panels<4, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
-    default: xmv_panels<8, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
+    default: xmv_panels<kPanelSlots, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
   }
 }
 
@@ -256,17 +318,17 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     const GraphDesc L = swap ? A : B;
     const int n = U.n, m = L.n, nm = n * m;
     const int SL = 2 * L.ne;
-    const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : 8);
+    const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : kPanelSlots);
 
     PairView v;
     v.urp = ds.rowptr + U.rowptr_off;
     v.ue = ds.rowent + U.nz_off;
     v.lrp = ds.rowptr + L.rowptr_off;
     v.le = ds.rowent + L.nz_off;
-    v.prow = ns == 8 ? ds.panel_row + L.panel_off : nullptr;
+    v.prow = SL > 128 ? ds.panel_row + L.panel_off : nullptr;
     v.n = n;
     v.m = m;
-    v.np = ns == 8 ? L.npanels : 1;
+    v.np = SL > 128 ? L.npanels : 1;
     {
       int rpc = (n * v.np) / (4 * kPW);
       rpc = rpc < 2 ? 2 : (rpc > 32 ? 32 : rpc);
@@ -573,16 +635,16 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     const GraphDesc L = swap ? A : B;
     const int n = U.n, m = L.n, nm = n * m;
     const int SL = 2 * L.ne;
-    const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : 8);
+    const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : kPanelSlots);
     PairView v;
     v.urp = ds.rowptr + U.rowptr_off;
     v.ue = ds.rowent + U.nz_off;
     v.lrp = ds.rowptr + L.rowptr_off;
     v.le = ds.rowent + L.nz_off;
-    v.prow = ns == 8 ? ds.panel_row + L.panel_off : nullptr;
+    v.prow = SL > 128 ? ds.panel_row + L.panel_off : nullptr;
     v.n = n;
     v.m = m;
-    v.np = ns == 8 ? L.npanels : 1;
+    v.np = SL > 128 ? L.npanels : 1;
     v.rpc = 8;
     const int64_t di = gthreads / m, dl = gthreads % m;
 

@@ -35,10 +35,17 @@ SIGNATURES = {
     "mgk_gram_shard": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, _P, _P, _P, _P, _P, _P]),
     "mgk_pairs": (C.c_int, [_P, C.c_int64, _P, _P, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
     "mgk_kernel": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
+    "mgk_gram_nodewise": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_int64, _P, _P, _P, _P]),
     "mgk_last_timing": (C.c_int, [_P, _P, _P]),
     "mgk_bench_peaks": (C.c_int, [C.c_int, _P, _P]),
     "mgk_transfer_bytes": (C.c_int, [_P, _P]),
 }
+
+
+# mgk_nodewise_sink (include/mgk.h)
+NODEWISE_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                            C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(C.c_uint8),
+                            C.POINTER(C.c_int64), C.POINTER(C.c_float))
 
 
 class NativeError(RuntimeError):
@@ -161,6 +168,36 @@ class Context:
         check(self.lib.mgk_gram_shard(self.h, rank, world, float(tol), int(max_iter), C.byref(n), _ptr(pa),
                                       _ptr(pb), _ptr(v), _ptr(it), _ptr(cv)))
         return pa, pb, v, it, cv
+
+    def gram_nodewise(self, rank: int, world: int, tol: float, consumer, chunk_bytes: int = 1 << 30,
+                      max_iter: int = 0):
+        """Stream this rank's Gram pairs with their nodewise fields to ``consumer(a, b, value, iterations,
+        converged, offsets, field)`` (numpy views valid during the call).  Returns (pairs, floats)."""
+        err = []
+
+        def cb(_user, k, pa, pb, val, it, cv, off, nw):
+            try:
+                a = np.ctypeslib.as_array(pa, (k,))
+                b = np.ctypeslib.as_array(pb, (k,))
+                v = np.ctypeslib.as_array(val, (k,))
+                i = np.ctypeslib.as_array(it, (k,))
+                c = np.ctypeslib.as_array(cv, (k,)).astype(bool)
+                o = np.ctypeslib.as_array(off, (k + 1,))
+                f = np.ctypeslib.as_array(nw, (int(o[-1]),)) if o[-1] > 0 else np.zeros(0, np.float32)
+                consumer(a, b, v, i, c, o, f)
+                return 0
+            except BaseException as e:  # surfaced after the C call returns
+                err.append(e)
+                return 1
+
+        fn = NODEWISE_SINK(cb)
+        n, f = C.c_int64(), C.c_int64()
+        rc = self.lib.mgk_gram_nodewise(self.h, int(rank), int(world), float(tol), int(max_iter), int(chunk_bytes),
+                                        C.cast(fn, C.c_void_p), None, C.byref(n), C.byref(f))
+        if err:
+            raise err[0]
+        check(rc)
+        return n.value, f.value
 
     def pairs(self, a, b, tol: float, max_iter: int = 0, nodewise: bool = False, sizes=None):
         a = np.ascontiguousarray(a, dtype=np.int32)

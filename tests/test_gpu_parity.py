@@ -203,6 +203,35 @@ def test_grid_class_vs_oracle(mgk, monkeypatch):
     _check_gram_vs_oracle(mgk, ul[:2], None, None, tol=1e-6)
 
 
+def test_stream_nodewise_vs_oracle(mgk):
+    """mgk_gram_nodewise: every pair a <= b of a mixed-size set (warp, tiny, panel classes), streamed in
+    several chunks and sharded over two ranks; fields and values against the oracle."""
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(21)
+    ds = [synth.molecule(rng, int(n)) for n in (5, 9, 14, 23, 30, 47)]
+    sizes = [g.node_count for g in ds]
+    seen = {}
+    chunks = []
+
+    def take(a, b, v, it, cv, off, f):
+        chunks.append(len(a))
+        for k in range(len(a)):
+            key = (int(a[k]), int(b[k]))
+            assert key not in seen
+            seen[key] = (float(v[k]), int(it[k]), bool(cv[k]),
+                         f[off[k]:off[k + 1]].reshape(sizes[a[k]], sizes[b[k]]).copy())
+
+    for rank in range(2):
+        mgk.stream_nodewise(ds, take, "delta:0.5", "se:1.0", chunk_bytes=4 * 1500, rank=rank, world=2)
+    assert sorted(seen) == [(a, b) for a in range(6) for b in range(a, 6)]
+    assert len(chunks) > 4
+    for (a, b), (v, it, cv, field) in seen.items():
+        o = O.solve_pcg(ds[a], ds[b], ("delta", 0.5), ("se", 1.0))
+        assert cv and abs(v - o.value) <= REL * abs(o.value) and abs(it - o.iterations) <= 1
+        assert np.max(np.abs(field - o.nodewise)) <= REL * np.max(np.abs(o.nodewise)), (a, b)
+
+
 def test_panel_unlabeled_rgg_vs_oracle(mgk):
     """Config-4 shape (random geometric graphs, unlabeled, tol 1e-6 per SURVEY H1) at reduced n."""
     from paper_1910_06310_b200 import synth
