@@ -59,6 +59,7 @@ class Config:
     cpu_pairs: int        # default oracle sample for cpu_baseline
     parity_pairs: int
     kernel: str           # dominant solver kernel
+    nodewise: bool = False  # stream every pair's nodal-similarity field (mgk_gram_nodewise)
 
 
 CONFIGS = {
@@ -75,7 +76,12 @@ CONFIGS = {
                   None, "se:1.0", 1e-10, 7, True, 0, 0, "k_pcg_grid<SE>"),
     "5": Config("5", "config5: {G} mixed-size synthetic molecules (60% n 4..23, 30% 24..64, 10% 65..128), "
                 "all-pairs Gram", "delta:0.5", "se:1.0", 1e-10, 7, False, 20000, 100, "k_pcg_warp + k_pcg_panel"),
+    "5nw": Config("5nw", "config5 nodal similarity: {G} mixed-size molecules, every pair's n_a x n_b field streamed "
+                  "to the host in 1 GiB chunks", "delta:0.5", "se:1.0", 1e-10, 7, False, 20000, 100,
+                  "k_pcg_warp<nodewise> + k_pcg_panel<nodewise>", nodewise=True),
 }
+
+NW_CHUNK = 1 << 30
 
 
 def buckets(cfg: Config, count: int | None):
@@ -88,7 +94,7 @@ def buckets(cfg: Config, count: int | None):
         return [("all", synth.config2(count=count or 7165))]
     if cfg.key == "3":
         return [("all", synth.config3(count=count or 1000))]
-    if cfg.key == "5":
+    if cfg.key in ("5", "5nw"):
         return [("all", synth.config5(count=count or 10000))]
     per = count or 25
     out = []
@@ -258,7 +264,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
 
     from paper_1910_06310_b200 import native
-    from paper_1910_06310_b200.gram import compute_gram
+    from paper_1910_06310_b200.gram import compute_gram, stream_nodewise
 
     cfg = CONFIGS[args.config]
     dist = None
@@ -290,6 +296,12 @@ def run_ours(args, rank, world, local_rank):
         """One Gram per bucket (N=1: device-resident result; N>1: shard + gather to rank 0)."""
         ms_tot, nl_tot, g_tot = 0.0, 0, 0.0
         for ctx, (_, ds) in zip(ctxs, bks):
+            if cfg.nodewise:
+                ctx.gram_nodewise(rank, world, cfg.tol, _discard, NW_CHUNK)
+                ms, launches = ctx.last_timing()
+                ms_tot += ms
+                nl_tot += launches
+                continue
             if world == 1:
                 ctx.gram(cfg.tol, fetch=False)
                 ms, launches = ctx.last_timing()
@@ -387,6 +399,11 @@ def run_ours(args, rank, world, local_rank):
             t0 = time.perf_counter()
             for _, ds in raw:
                 src = reorder_dataset(ds, local_rank) if cfg.reorder else ds
+                if cfg.nodewise:
+                    got = stream_nodewise(src, _checksum, cfg.vspec, cfg.espec, _solver_cfg(cfg), NW_CHUNK,
+                                          device=local_rank)
+                    assert got[0] == len(ds) * (len(ds) + 1) // 2
+                    continue
                 res = compute_gram(src, cfg.vspec, cfg.espec, cfg=_solver_cfg(cfg), device=local_rank)
                 assert res.matrix.shape == (len(ds), len(ds))
             torch.cuda.synchronize(dev)
@@ -450,8 +467,11 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": (h1 - h0) // nrep,
                 "d2h_bytes_per_step": (d1 - d0) // nrep,
                 "ms_per_step": float(np.mean(e2e_ms)),
-                "api": "paper_1910_06310_b200.compute_gram (validate, pack, C-ABI upload, device octiles, solve, "
-                       "D2H of the N x N matrix, iterations and flags)"
+                "api": ("paper_1910_06310_b200.stream_nodewise (validate, pack, C-ABI upload, device octiles, "
+                        "chunked solve, D2H of every pair's field into pinned buffers, host checksum of each chunk)"
+                        if cfg.nodewise else
+                        "paper_1910_06310_b200.compute_gram (validate, pack, C-ABI upload, device octiles, solve, "
+                        "D2H of the N x N matrix, iterations and flags)")
                        + (" after pbr_reorder_many + apply_permutation" if cfg.reorder else ""),
             },
             "gpu_launches": launches,
@@ -466,6 +486,18 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def _discard(*_chunk):
+    """Device-timed nodewise leg: the fields reach pinned host memory and are dropped."""
+
+
+_NW_SUM = [0.0]
+
+
+def _checksum(a, b, v, it, cv, off, field):
+    """End-to-end nodewise leg: touch every streamed field (a float64 sum over the chunk)."""
+    _NW_SUM[0] += float(np.sum(field, dtype=np.float64))
 
 
 def _solver_cfg(cfg: Config):

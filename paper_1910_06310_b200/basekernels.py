@@ -102,9 +102,28 @@ class CompactPolynomial(BaseKernel):
         return K_POLY, list(self.coeffs)
 
 
+SCALAR_KERNELS = (ConstantOne, KroneckerDelta, SquareExponential, CompactPolynomial)
+MAX_COMPONENTS = 4
+
+
+def _scalar_spec(k: BaseKernel) -> str:
+    if isinstance(k, ConstantOne):
+        return "const1"
+    if isinstance(k, KroneckerDelta):
+        return f"delta:{k.h!r}"
+    if isinstance(k, SquareExponential):
+        return f"se:{k.alpha!r}"
+    if isinstance(k, CompactPolynomial):
+        k.device_descriptor()  # raises for unsupported variants
+        return "poly:" + ",".join(repr(c) for c in k.coeffs)
+    raise NotImplementedError(f"{type(k).__name__} is not a scalar kernel; the device composes scalar kernels only")
+
+
 @dataclass
 class ProductComposite(BaseKernel):
-    """Component-wise product (basekernels.py:175-211); device lowering pending."""
+    """Product of one scalar sub-kernel per label component (basekernels.py:175-211).
+
+    Lowers to the device spec ``prod:K1|K2|...`` (evaluated in-kernel, csrc/mgk_dev.cuh)."""
 
     components: Sequence[BaseKernel]
 
@@ -112,20 +131,37 @@ class ProductComposite(BaseKernel):
         self.components = tuple(self.components)
         self.flop_count = sum(k.flop_count for k in self.components) + max(len(self.components) - 1, 0)
 
+    def spec(self) -> str:
+        if not 1 <= len(self.components) <= MAX_COMPONENTS:
+            raise NotImplementedError(f"1..{MAX_COMPONENTS} composite components on device")
+        if sum(isinstance(k, CompactPolynomial) for k in self.components) > 1:
+            raise NotImplementedError("at most one polynomial component on device")
+        return "prod:" + "|".join(_scalar_spec(k) for k in self.components)
+
 
 @dataclass
 class RConvolution(BaseKernel):
-    """Sum over component pairs (basekernels.py:214-244); device lowering pending."""
+    """sum_i sum_j inner(a_i, b_j) over label components (basekernels.py:214-244).
+
+    Lowers to the device spec ``rconv:K`` (evaluated in-kernel, csrc/mgk_dev.cuh)."""
 
     inner: BaseKernel
 
     def __post_init__(self):
         self.flop_count = self.inner.flop_count + 1
 
+    def spec(self) -> str:
+        return "rconv:" + _scalar_spec(self.inner)
+
 
 def kernel_from_spec(spec: str) -> BaseKernel:
-    """``const1 | delta:H | se:ALPHA | poly:C0,C1,...`` (basekernels.py:247-261)."""
+    """``const1 | delta:H | se:ALPHA | poly:C0,C1,...`` (basekernels.py:247-261), plus the
+    composite forms ``prod:K1|K2|...`` and ``rconv:K`` of the class-only kernels."""
     head, _, rest = spec.partition(":")
+    if head == "prod":
+        return ProductComposite([kernel_from_spec(p) for p in rest.split("|")])
+    if head == "rconv":
+        return RConvolution(kernel_from_spec(rest))
     if head == "const1":
         return ConstantOne()
     if head == "delta":

@@ -77,7 +77,45 @@ struct Spec {
   int kind = KK_NONE;  // KK_NONE == None
   double h = 1.0, alpha = 1.0;
   std::vector<double> coef;
+  std::vector<Spec> sub;  // PROD components / RCONV inner kernel
 };
+
+int parse_spec(const char* s, Spec& out);
+
+// Composite grammar (extension of basekernels.py:247-261 for the class-only kernels):
+//   prod:K1|K2|...   ProductComposite(K1, K2, ...)   (basekernels.py:175-211)
+//   rconv:K          RConvolution(K)                 (basekernels.py:214-244)
+// with scalar sub-kernels K in const1 | delta:H | se:A | poly:c0,..
+static int parse_composite(const std::string& head, const std::string& rest, Spec& out) {
+  std::vector<std::string> parts;
+  if (head == "prod") {
+    size_t pos = 0;
+    for (;;) {
+      size_t bar = rest.find('|', pos);
+      parts.push_back(rest.substr(pos, bar == std::string::npos ? std::string::npos : bar - pos));
+      if (bar == std::string::npos) break;
+      pos = bar + 1;
+    }
+    out.kind = KK_PROD;
+  } else {
+    parts.push_back(rest);
+    out.kind = KK_RCONV;
+  }
+  if ((int)parts.size() > kMaxSub)
+    return fail(MGK_E_UNSUPPORTED, "at most %d composite components on device", kMaxSub);
+  int polys = 0;
+  for (const std::string& p : parts) {
+    Spec sub;
+    int rc = parse_spec(p.c_str(), sub);
+    if (rc) return rc;
+    if (sub.kind == KK_NONE || sub.kind == KK_PROD || sub.kind == KK_RCONV)
+      return fail(MGK_E_UNSUPPORTED, "composite components must be scalar kernels, got '%s'", p.c_str());
+    if (sub.kind == KK_POLY && ++polys > 1)
+      return fail(MGK_E_UNSUPPORTED, "at most one polynomial component on device");
+    out.sub.push_back(sub);
+  }
+  return MGK_OK;
+}
 
 int parse_spec(const char* s, Spec& out) {
   out = Spec();
@@ -86,6 +124,7 @@ int parse_spec(const char* s, Spec& out) {
   auto colon = str.find(':');
   std::string head = str.substr(0, colon);
   std::string rest = colon == std::string::npos ? "" : str.substr(colon + 1);
+  if (head == "prod" || head == "rconv") return parse_composite(head, rest, out);
   try {
     if (head == "const1") {
       out.kind = KK_CONST1;
@@ -126,6 +165,15 @@ KernelDesc to_desc(const Spec& s) {
   d.se_scale = (float)std::sqrt(s.alpha * 1.4426950408889634);
   d.ncoef = (int)s.coef.size();
   for (int i = 0; i < d.ncoef; ++i) d.coef[i] = (float)s.coef[i];
+  d.nsub = (int)s.sub.size();
+  for (int c = 0; c < d.nsub; ++c) {
+    d.sub_kind[c] = s.sub[c].kind;
+    d.sub_h[c] = (float)s.sub[c].h;
+    if (s.sub[c].kind == KK_POLY) {
+      d.ncoef = (int)s.sub[c].coef.size();
+      for (int i = 0; i < d.ncoef; ++i) d.coef[i] = (float)s.sub[c].coef[i];
+    }
+  }
   return d;
 }
 
@@ -136,10 +184,45 @@ struct Lowered {
   std::vector<float> data;
 };
 
+// Composite kernels: every component lowered for its scalar sub-kernel.
+static int lower_composite(int kind, int dim, const std::vector<int64_t>& cat, const std::vector<double>& vec,
+                           size_t count, const Spec& k, Lowered& out) {
+  if (kind == LK_CAT) dim = 1;
+  auto raw = [&](size_t i, int c) { return kind == LK_CAT ? (double)cat[i] : vec[i * dim + c]; };
+  if (k.kind == KK_PROD && dim != (int)k.sub.size())
+    return fail(MGK_E_SHAPE, "composite kernel component count mismatch: %d components, labels of dimension %d",
+                (int)k.sub.size(), dim);
+  if (dim > kMaxLabelDim) return fail(MGK_E_UNSUPPORTED, "label dimension %d > %d", dim, kMaxLabelDim);
+  out.kind = LK_VEC;
+  out.dim = dim;
+  out.data.assign(count * dim, 0.0f);
+  // RCONV compares every component with every component: one class map / scale for all of them
+  for (int c = 0; c < dim; ++c) {
+    const Spec& sub = k.kind == KK_PROD ? k.sub[c] : k.sub[0];
+    if (sub.kind == KK_DELTA) {
+      if (k.kind == KK_RCONV && c > 0) continue;  // filled below with the shared map
+      std::map<double, int32_t> ids;
+      const int c0 = c, c1 = k.kind == KK_RCONV ? dim : c + 1;
+      for (size_t i = 0; i < count; ++i)
+        for (int cc = c0; cc < c1; ++cc) {
+          double key = raw(i, cc);
+          if (key == 0.0) key = 0.0;
+          int32_t v = ids.emplace(key, (int32_t)ids.size()).first->second;
+          memcpy(&out.data[i * dim + cc], &v, 4);
+        }
+    } else {
+      const double scale = sub.kind == KK_SE ? std::sqrt(sub.alpha * 1.4426950408889634) : 1.0;
+      for (size_t i = 0; i < count; ++i) out.data[i * dim + c] = (float)(raw(i, c) * scale);
+    }
+  }
+  return MGK_OK;
+}
+
 int lower_labels(int kind, int dim, const std::vector<int64_t>& cat, const std::vector<double>& vec, size_t count,
                  const Spec& k, Lowered& out, const char* what) {
   out = Lowered();
   if (kind == LK_NONE || k.kind == KK_NONE || k.kind == KK_CONST1) return MGK_OK;
+  if (k.kind == KK_PROD || k.kind == KK_RCONV) return lower_composite(kind, dim, cat, vec, count, k, out);
   if (k.kind == KK_DELTA) {
     // equality classes -> dense ids: exact for int64 tokens and float vectors alike
     out.kind = LK_CAT;
@@ -221,10 +304,10 @@ struct mgk_ctx {
   DBuf<float> d_resid, d_scratch, d_nodewise, d_gridvec;
   DBuf<double2> d_gridbuf;
   DBuf<int64_t> d_nwoff;
-  DBuf<int32_t> d_pa, d_pb, d_rowcol;
+  DBuf<int32_t> d_pa, d_pb, d_rowcol, d_wide;
   DBuf<int64_t> d_rowpre;
   // host images of the Gram job lists (host-side pair decoding for streaming)
-  std::vector<int32_t> h_lists, h_rowcol;
+  std::vector<int32_t> h_lists, h_rowcol, h_wide;
   std::vector<int64_t> h_rowpre;
   // pinned staging for streamed nodewise chunks
   float* h_nw = nullptr;
@@ -608,8 +691,13 @@ int mgk_degrees(mgk_ctx* c, int32_t g, double* d_out) {
 // Solver dispatch
 // ---------------------------------------------------------------------------
 
+// composite edge kernels (vector labels, per-component sub-kernels) run on the generic CTA solver
+static bool composite_edges(const mgk_ctx* c) {
+  return c->el_kind != LK_NONE && (c->espec.kind == KK_PROD || c->espec.kind == KK_RCONV);
+}
+
 static bool small_graph(const mgk_ctx* c, const GraphDesc& d) {
-  return d.n <= SmallClass::NU && 2 * d.ne <= SmallClass::SMAX && c->ds.el_dim <= 1;
+  return d.n <= SmallClass::NU && 2 * d.ne <= SmallClass::SMAX && c->ds.el_dim <= 1 && !composite_edges(c);
 }
 
 // n * m at or below which a small pair is solved by the FP64 tiny kernel
@@ -634,6 +722,7 @@ enum JobKernel { JK_BLOCK = 0, JK_WARP = 1, JK_TINY = 2, JK_PANEL = 3, JK_GRID =
 struct JobSpec {
   PairJob job;
   int kernel;         // JobKernel
+  int slots = SmallClass::SLOTS;  // warp solver lane-slot capacity
   int64_t max_n, max_m, max_su, max_sl;
 };
 
@@ -641,7 +730,7 @@ struct JobSpec {
 // Panel solver eligibility: scalar edge labels and row panels for every graph
 // (a row of more than kPanelCap nonzeros sends the dataset to the block kernel).
 static bool panel_dataset(const mgk_ctx* c) {
-  if (c->ds.el_dim > 1) return false;
+  if (c->ds.el_dim > 1 || composite_edges(c)) return false;
   if (getenv("MGK_NO_PANEL")) return false;
   for (const GraphDesc& d : c->graphs)
     if (d.npanels <= 0) return false;
@@ -724,7 +813,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     if (o.pair_b) o.pair_b += off;
     cudaError_t e;
     if (j.kernel == JK_WARP)
-      e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
+      e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, j.slots, s);
     else if (j.kernel == JK_TINY)
       e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
     else if (j.kernel == JK_GRID)
@@ -834,16 +923,35 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
     return j;
   };
   const int cta = panel ? JK_PANEL : JK_BLOCK;
+  // pairs of two wide small graphs (> 32 * kNarrowSlots nonzeros each) leave the narrow warp
+  // instantiation (it skips them) for an explicit list on the wide one
+  std::vector<int32_t> wide;
+  for (int32_t g : small)
+    if ((2 * c->graphs[g].ne + 31) / 32 > kNarrowSlots) wide.push_back(g);
+  std::sort(wide.begin(), wide.end());
+  std::vector<int32_t> wl;
+  for (size_t x = 0; x < wide.size(); ++x)
+    for (size_t y = x; y < wide.size(); ++y) wl.push_back(wide[x]);
+  for (size_t x = 0; x < wide.size(); ++x)
+    for (size_t y = x; y < wide.size(); ++y) wl.push_back(wide[y]);
+  const int64_t nwide = (int64_t)wl.size() / 2;
+  CUDA_TRY(c->d_wide.upload(wl, s));
+  c->h_wide = wl;
+  JobSpec jw{};
+  jw.job = PairJob{PM_LIST, 0, 0, nwide, 0, 1, c->d_wide.ptr, c->d_wide.ptr + nwide, nullptr, nullptr};
+  jw.kernel = JK_WARP;
+  jw.slots = SmallClass::SLOTS;
   JobSpec jm{};
   jm.job = PairJob{PM_RAGGED, (int32_t)ns, 0, mpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr, c->d_rowcol.ptr};
   jm.kernel = JK_WARP;
+  jm.slots = kNarrowSlots;
   JobSpec jt{};
   jt.job = PairJob{PM_RAGGED, (int32_t)ns, 0, tpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr + ns + 1,
                    c->d_rowcol.ptr + ns};
   jt.kernel = JK_TINY;
   // big pairs first (longest job first across classes)
   jobs = {tri(large, dlarge, JK_GRID), rect(large, dlarge, mid, dmid, cta), rect(large, dlarge, small, dsmall, cta),
-          tri(mid, dmid, cta), rect(mid, dmid, small, dsmall, cta), jm, jt};
+          tri(mid, dmid, cta), rect(mid, dmid, small, dsmall, cta), jw, jm, jt};
   return MGK_OK;
 }
 
@@ -926,8 +1034,9 @@ static PairJob host_job(const mgk_ctx* c, const PairJob& j) {
   auto rebase32 = [&](const int32_t* p, const DBuf<int32_t>& d, const std::vector<int32_t>& hv) -> const int32_t* {
     return p ? hv.data() + (p - d.ptr) : nullptr;
   };
-  h.list_a = rebase32(j.list_a, c->d_list_a, c->h_lists);
-  h.list_b = rebase32(j.list_b, c->d_list_a, c->h_lists);
+  const bool wide = j.list_a && j.list_a >= c->d_wide.ptr && j.list_a < c->d_wide.ptr + c->d_wide.n;
+  h.list_a = wide ? rebase32(j.list_a, c->d_wide, c->h_wide) : rebase32(j.list_a, c->d_list_a, c->h_lists);
+  h.list_b = wide ? rebase32(j.list_b, c->d_wide, c->h_wide) : rebase32(j.list_b, c->d_list_a, c->h_lists);
   h.row_col0 = rebase32(j.row_col0, c->d_rowcol, c->h_rowcol);
   h.row_prefix = j.row_prefix ? c->h_rowpre.data() + (j.row_prefix - c->d_rowpre.ptr) : nullptr;
   return h;

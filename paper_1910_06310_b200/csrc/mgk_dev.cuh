@@ -60,9 +60,14 @@ struct GraphDesc {
 constexpr int kPanelSlots = MGK_PANEL_SLOTS;
 constexpr int kPanelCap = 32 * kPanelSlots;
 
-// Base-kernel descriptor (basekernels.py:60-172); kind codes match basekernels.py.
-enum KernelKind : int32_t { KK_CONST1 = 0, KK_DELTA = 1, KK_SE = 2, KK_POLY = 3, KK_NONE = 4 };
+// Base-kernel descriptor (basekernels.py:60-244); kind codes match basekernels.py.
+// KK_PROD = ProductComposite (one scalar sub-kernel per label component,
+// basekernels.py:175-211), KK_RCONV = RConvolution (sum of a scalar inner
+// kernel over all component pairs, basekernels.py:214-244).
+enum KernelKind : int32_t { KK_CONST1 = 0, KK_DELTA = 1, KK_SE = 2, KK_POLY = 3, KK_NONE = 4, KK_PROD = 5,
+                            KK_RCONV = 6 };
 constexpr int kMaxPoly = 8;
+constexpr int kMaxSub = 4;
 struct KernelDesc {
   int32_t kind;
   int32_t ncoef;
@@ -70,6 +75,9 @@ struct KernelDesc {
   float alpha;         // SE alpha
   float se_scale;      // sqrt(alpha * log2(e)): labels are pre-scaled so SE = exp2(-|a-b|^2)
   float coef[kMaxPoly];
+  int32_t nsub;                 // PROD: components; RCONV: 1 (the inner kernel)
+  int32_t sub_kind[kMaxSub];    // scalar kinds (CONST1 / DELTA / SE / POLY; POLY uses coef)
+  float sub_h[kMaxSub];         // delta baselines
 };
 
 
@@ -142,10 +150,42 @@ __device__ __forceinline__ float kernel_scalar(const KernelDesc& k, float a, flo
   }
 }
 
+// Scalar sub-kernel c of a composite / convolution descriptor on lowered labels
+// (delta components are equivalence-class ids, SE components pre-scaled).
+__device__ __forceinline__ float sub_kernel(const KernelDesc& k, int c, float a, float b) {
+  switch (k.sub_kind[c]) {
+    case KK_DELTA:
+      return (__float_as_int(a) == __float_as_int(b)) ? 1.0f : k.sub_h[c];
+    case KK_SE: {
+      float d = a - b;
+      return exp2f(-d * d);
+    }
+    case KK_POLY: {
+      float d = fabsf(a - b);
+      float acc = 0.0f;
+      for (int i = k.ncoef - 1; i >= 0; --i) acc = fmaf(acc, d, k.coef[i]);
+      return fminf(fmaxf(acc, 0.0f), 1.0f);
+    }
+    default:
+      return 1.0f;
+  }
+}
+
 // Vector-label version (dim <= kMaxLabelDim); categorical labels compare as ints.
 __device__ __forceinline__ float kernel_vec(const KernelDesc& k, const float* a, const float* b, int dim,
                                             bool categorical) {
   switch (k.kind) {
+    case KK_PROD: {
+      float out = 1.0f;
+      for (int c = 0; c < k.nsub; ++c) out *= sub_kernel(k, c, a[c], b[c]);
+      return out;
+    }
+    case KK_RCONV: {
+      float s = 0.0f;
+      for (int i = 0; i < dim; ++i)
+        for (int j = 0; j < dim; ++j) s += sub_kernel(k, 0, a[i], b[j]);
+      return s;
+    }
     case KK_DELTA: {
       bool eq = true;
       if (categorical) {

@@ -121,10 +121,12 @@ struct SmallClass {
   static constexpr int SLOTS = 10;   // lane-side nonzeros <= 32 * SLOTS
   static constexpr int SMAX = 32 * SLOTS;
 };
+// narrow warp-solver instantiation: lane graphs of <= 32 * kNarrowSlots nonzeros
+constexpr int kNarrowSlots = 4;
 
 cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
-                            int num_sms, cudaStream_t stream);
+                            int num_sms, int slots, cudaStream_t stream);
 cudaError_t launch_pcg_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                             int num_sms, cudaStream_t stream);

@@ -94,15 +94,15 @@ __device__ void block_octiles_to_rows(const DatasetDev& ds, const GraphDesc& g, 
 __device__ __forceinline__ float block_kappa(const KernelDesc& ek, int kind, const float4& a, const float4& b,
                                              const float* ax, const float* bx, int el_dim, bool cat) {
   if (kind == KK_NONE) return 1.0f;
-  if (el_dim <= 1) {
+  if (el_dim <= 1 && kind != KK_PROD && kind != KK_RCONV) {
     if (kind == KK_DELTA) return (__float_as_int(a.z) == __float_as_int(b.z)) ? 1.0f : ek.h;
     return kernel_scalar(ek, a.z, b.z);
   }
   float la[kMaxLabelDim], lb[kMaxLabelDim];
   la[0] = a.z;
-  la[1] = a.w;
+  la[1] = el_dim > 1 ? a.w : 0.0f;
   lb[0] = b.z;
-  lb[1] = b.w;
+  lb[1] = el_dim > 1 ? b.w : 0.0f;
   for (int d = 2; d < el_dim; ++d) {
     la[d] = ax[d];
     lb[d] = bx[d];

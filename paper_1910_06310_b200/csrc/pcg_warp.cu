@@ -42,17 +42,17 @@ constexpr int NU = SmallClass::NU;
 constexpr int SLOTS = SmallClass::SLOTS;
 constexpr int SMAX = SmallClass::SMAX;
 
-template <bool UNLAB, bool NODEWISE>
+// Per-warp shared memory.  The residual and the diagonal live in registers
+// (lane = L node, one register per U row), so only the XMV operands are here.
+template <bool UNLAB, bool NODEWISE, int SLM>
 struct WarpSmem {
   float P[NU][32];        // P + OFF: staging area for the L nonzeros during the prologue
   float OFF[NU][32];
-  float R[NU][32];        // residual
-  float DG[NU][32];       // diagonal d_i d'_l / kv
   float T[UNLAB ? NU : 1][32];
   float X[NODEWISE ? NU : 1][32];
   float2 UWL[SMAX];       // U nonzeros in row order: {w, label}
   int UOFF[SMAX];         //   and the byte offset of P row j (j * 128)
-  float SEG[2 * 32 * SLOTS];  // segment sums of two U-rows
+  float SEG[2 * 32 * SLM];  // segment sums of two U-rows
   int urow[NU + 8];
   int lrow[40];
   float upq[NU];          // p_i of U nodes
@@ -271,9 +271,9 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
 // XMV, labeled: OFF[i][l] for all U-rows i, NS slots per lane.
 // ---------------------------------------------------------------------------
 // acc[t] += sum_{k in U(i)} kappa(e_k, e'_t) w_k P[j_k][col_L(t)]  (row i of U)
-template <int NS, int EK, class Smem>
+template <int NS, int EK, int SLM, class Smem>
 __device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& ek, int i, const char* pbase,
-                                               const int (&lcoff)[SLOTS], const float (&llab)[SLOTS],
+                                               const int (&lcoff)[SLM], const float (&llab)[SLM],
                                                float (&acc)[NS]) {
   const int k1 = S.urow[i + 1];
   int k = S.urow[i];
@@ -305,22 +305,22 @@ __device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& 
 
 // Two U-rows per pass: one SEG round trip and one pair of warp syncs per two
 // rows, and two independent summation chains in the segment reduction.
-template <int NS, int EK, class Smem>
+template <int NS, int EK, int SLM, class Smem>
 __device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int nu, int m, int lane,
-                                            const int (&lcoff)[SLOTS], const float (&lw)[SLOTS],
-                                            const float (&llab)[SLOTS], int lr0, int lr1) {
+                                            const int (&lcoff)[SLM], const float (&lw)[SLM],
+                                            const float (&llab)[SLM], int lr0, int lr1) {
   const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
   for (int i = 0; i < nu; i += 2) {
     const bool two = i + 1 < nu;
     float acc0[NS], acc1[NS];
 #pragma unroll
     for (int t = 0; t < NS; ++t) acc0[t] = acc1[t] = 0.0f;
-    accumulate_row<NS, EK>(S, ek, i, pbase, lcoff, llab, acc0);
-    if (two) accumulate_row<NS, EK>(S, ek, i + 1, pbase, lcoff, llab, acc1);
+    accumulate_row<NS, EK, SLM>(S, ek, i, pbase, lcoff, llab, acc0);
+    if (two) accumulate_row<NS, EK, SLM>(S, ek, i + 1, pbase, lcoff, llab, acc1);
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
       S.SEG[lane + 32 * t] = acc0[t] * lw[t];
-      S.SEG[32 * SLOTS + lane + 32 * t] = acc1[t] * lw[t];
+      S.SEG[32 * SLM + lane + 32 * t] = acc1[t] * lw[t];
     }
     __syncwarp();
     if (lane < m) {
@@ -328,7 +328,7 @@ __device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int n
 #pragma unroll 2
       for (int q = lr0; q < lr1; ++q) {
         s0 += S.SEG[q];
-        s1 += S.SEG[32 * SLOTS + q];
+        s1 += S.SEG[32 * SLM + q];
       }
       S.OFF[i][lane] = s0;
       if (two) S.OFF[i + 1][lane] = s1;
@@ -338,9 +338,9 @@ __device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int n
 }
 
 // XMV, unlabeled (kappa = 1): T = P B^T (slots + segment sums), OFF = A T.
-template <int NS, class Smem>
-__device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, const int (&lcoff)[SLOTS],
-                                              const float (&lw)[SLOTS], int lr0, int lr1) {
+template <int NS, int SLM, class Smem>
+__device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, const int (&lcoff)[SLM],
+                                              const float (&lw)[SLM], int lr0, int lr1) {
   const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
   for (int j = 0; j < nu; ++j) {
     const char* row = pbase + j * 128;
@@ -363,16 +363,18 @@ __device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, 
   __syncwarp();
 }
 
-template <int EK, class Smem>
+template <int EK, int SLM, class Smem>
 __device__ __forceinline__ void xmv_dispatch(int ns, Smem& S, const KernelDesc& ek, int nu, int m, int lane,
-                                             const int (&lcoff)[SLOTS], const float (&lw)[SLOTS],
-                                             const float (&llab)[SLOTS], int lr0, int lr1) {
-#define MGK_XMV_CASE(N)                                                     \
-  case N:                                                                   \
-    if constexpr (EK == KK_NONE)                                            \
-      xmv_unlabeled<N>(S, nu, m, lane, lcoff, lw, lr0, lr1);                \
-    else                                                                    \
-      xmv_labeled<N, EK>(S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);    \
+                                             const int (&lcoff)[SLM], const float (&lw)[SLM],
+                                             const float (&llab)[SLM], int lr0, int lr1) {
+#define MGK_XMV_CASE(N)                                                          \
+  case N:                                                                        \
+    if constexpr (N <= SLM) {                                                    \
+      if constexpr (EK == KK_NONE)                                               \
+        xmv_unlabeled<N, SLM>(S, nu, m, lane, lcoff, lw, lr0, lr1);              \
+      else                                                                       \
+        xmv_labeled<N, EK, SLM>(S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);  \
+    }                                                                            \
     break;
   switch (ns) {
     MGK_XMV_CASE(1)
@@ -390,15 +392,19 @@ __device__ __forceinline__ void xmv_dispatch(int ns, Smem& S, const KernelDesc& 
       __syncwarp();
   }
 #undef MGK_XMV_CASE
-  static_assert(SLOTS == 10, "xmv_dispatch covers 1..10 slots");
+  static_assert(SLOTS == 10 && SLM <= SLOTS, "xmv_dispatch covers 1..10 slots");
 }
 
-template <int EK, bool NODEWISE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 6)
+// SLM: lane-side slot capacity of this instantiation.  SLM = 4 (S_L <= 128)
+// covers ~95% of QM7-shaped pairs with a third of the registers; it skips the
+// pairs whose graphs both exceed 128 nonzeros, which the host routes to the
+// SLM = 10 instantiation as an explicit list.
+template <int EK, bool NODEWISE, int SLM>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, SLM <= 4 ? 8 : 6)
 k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
            unsigned long long* queue) {
   constexpr bool UNLAB = (EK == KK_NONE);
-  using Smem = WarpSmem<UNLAB, NODEWISE>;
+  using Smem = WarpSmem<UNLAB, NODEWISE, SLM>;
   static_assert(sizeof(float) * 2 * NU * 32 >= sizeof(float4) * SMAX, "staging area too small");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -415,11 +421,16 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int32_t ga, gb;
     decode_pair(job, (int64_t)pid, ga, gb);
     const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
-    // orientation: L takes the graph that minimises S_U * ceil(S_L / 32)
+    // orientation: L takes the graph that minimises S_U * ceil(S_L / 32), within SLM slots
     const int SA = 2 * A.ne, SB = 2 * B.ne;
-    const long costAB = (long)SA * ((SB + 31) / 32) + A.n;  // U = A, L = B
-    const long costBA = (long)SB * ((SA + 31) / 32) + B.n;
-    const bool swap = (costBA < costAB);
+    const int nsA = (SA + 31) >> 5, nsB = (SB + 31) >> 5;
+    const long costAB = (long)SA * nsB + A.n;  // U = A, L = B
+    const long costBA = (long)SB * nsA + B.n;
+    bool swap = (costBA < costAB);
+    if (SLM < SLOTS) {
+      if ((swap ? nsA : nsB) > SLM) swap = !swap;
+      if ((swap ? nsA : nsB) > SLM) continue;  // both graphs too wide: the SLM = 10 list has this pair
+    }
     const GraphDesc U = swap ? B : A;
     const GraphDesc L = swap ? A : B;
     const int nu = U.n, m = L.n;
@@ -435,10 +446,10 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       stage[pos] = make_float4(__int_as_float(col), w, lab, 0.0f);
     });
     __syncwarp();
-    int lcoff[SLOTS];
-    float lw[SLOTS], llab[SLOTS];
+    int lcoff[SLM];
+    float lw[SLM], llab[SLM];
 #pragma unroll
-    for (int t = 0; t < SLOTS; ++t) {
+    for (int t = 0; t < SLM; ++t) {
       const int k = lane + 32 * t;
       lcoff[t] = 0;
       lw[t] = 0.0f;
@@ -480,22 +491,26 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     const int64_t max_iter = prm.max_iter > 0 ? prm.max_iter : 10ll * nu * m;
     __syncwarp();
 
-    // x = 0, r = b, z = r / diag, p = z  (solver.py:91-97)
+    // x = 0, r = b, z = r / diag, p = z  (solver.py:91-97); R and diag in registers
+    const bool active = lane < m;
+    float rv[NU], dv[NU];
     double rho = 0.0, rr = 0.0;
-#pragma unroll 1
-    for (int i = 0; i < nu; ++i) {
-      float p0 = 0.0f;
-      if (lane < m) {
-        const float d = (float)diag_of(ds, vk, prm, vlab, U.node_off + i, L.node_off + lane);
-        const float r0 = (float)((double)S.udq[i] * ldq);
-        S.DG[i][lane] = d;
-        S.R[i][lane] = r0;
-        p0 = r0 * rcp_approx(d);
-        rho += (double)r0 * (double)p0;
-        rr += (double)r0 * (double)r0;
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      rv[i] = 0.0f;
+      dv[i] = 1.0f;
+      if (i < nu) {
+        float p0 = 0.0f;
+        if (active) {
+          dv[i] = (float)diag_of(ds, vk, prm, vlab, U.node_off + i, L.node_off + lane);
+          rv[i] = (float)((double)S.udq[i] * ldq);
+          p0 = rv[i] * rcp_approx(dv[i]);
+          rho += (double)rv[i] * (double)p0;
+          rr += (double)rv[i] * (double)rv[i];
+        }
+        S.P[i][lane] = p0;
+        if constexpr (NODEWISE) S.X[i][lane] = 0.0f;
       }
-      S.P[i][lane] = p0;
-      if constexpr (NODEWISE) S.X[i][lane] = 0.0f;
     }
     rho = warp_sum(rho);
     rr = warp_sum(rr);
@@ -503,12 +518,11 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int64_t it = 0;
     double value = 0.0;
     const bool self_pair = (ga == gb);
-    const bool active = lane < m;
     __syncwarp();
 
     while (!conv && it < max_iter) {
       // ---------------- off-diagonal product OFF = (A (x) A' . ke) P
-      xmv_dispatch<EK>(ns, S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);
+      xmv_dispatch<EK, SLM>(ns, S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);
       if (self_pair) {
         // self pair: the exact operator maps symmetric fields to symmetric fields;
         // symmetrising keeps the FP32 Krylov space in that subspace as the FP64
@@ -523,11 +537,11 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       ++it;
       // ---------------- PCG update (solver.py:98-110); A p = diag * p - OFF
       double pap = 0.0, pxp = 0.0;
-      if (active) {
-#pragma unroll 2
-        for (int i = 0; i < nu; ++i) {
+#pragma unroll
+      for (int i = 0; i < NU; ++i) {
+        if (i < nu && active) {
           const float p = S.P[i][lane];
-          const float ap = fmaf(S.DG[i][lane], p, -S.OFF[i][lane]);
+          const float ap = fmaf(dv[i], p, -S.OFF[i][lane]);
           S.OFF[i][lane] = ap;
           pap += (double)p * (double)ap;
           pxp += (double)S.upq[i] * (double)p;
@@ -539,13 +553,13 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       value += alpha * pxp;  // px . x accumulated as sum_k alpha_k (px . p_k)
       const float af = (float)alpha;
       double rr_l = 0.0, rz_l = 0.0;
-      if (active) {
-#pragma unroll 2
-        for (int i = 0; i < nu; ++i) {
+#pragma unroll
+      for (int i = 0; i < NU; ++i) {
+        if (i < nu && active) {
           if constexpr (NODEWISE) S.X[i][lane] = fmaf(af, S.P[i][lane], S.X[i][lane]);
-          const float r = fmaf(-af, S.OFF[i][lane], S.R[i][lane]);
-          const float z = r * rcp_approx(S.DG[i][lane]);
-          S.R[i][lane] = r;
+          const float r = fmaf(-af, S.OFF[i][lane], rv[i]);
+          const float z = r * rcp_approx(dv[i]);
+          rv[i] = r;
           S.OFF[i][lane] = z;
           rr_l += (double)r * (double)r;
           rz_l += (double)r * (double)z;
@@ -658,12 +672,12 @@ cudaError_t launch_pcg_tiny(const DatasetDev& ds, const KernelDesc& vk, const Ke
   }
 }
 
-template <int EK, bool NODEWISE>
+template <int EK, bool NODEWISE, int SLM>
 static cudaError_t launch_ek(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                              const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
                              cudaStream_t stream) {
-  using Smem = WarpSmem<EK == KK_NONE, NODEWISE>;
-  auto kern = k_pcg_warp<EK, NODEWISE>;
+  using Smem = WarpSmem<EK == KK_NONE, NODEWISE, SLM>;
+  auto kern = k_pcg_warp<EK, NODEWISE, SLM>;
   const size_t smem = sizeof(Smem) * kWarpsPerBlock;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -679,25 +693,29 @@ static cudaError_t launch_ek(const DatasetDev& ds, const KernelDesc& vk, const K
   return cudaGetLastError();
 }
 
-template <bool NODEWISE>
+template <bool NODEWISE, int SLM>
 static cudaError_t launch_nw(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                              const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
                              cudaStream_t stream) {
   int kind = prm.labeled ? ek.kind : KK_NONE;
   if (kind == KK_CONST1) kind = KK_NONE;
   switch (kind) {
-    case KK_SE: return launch_ek<KK_SE, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
-    case KK_DELTA: return launch_ek<KK_DELTA, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
-    case KK_POLY: return launch_ek<KK_POLY, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
-    default: return launch_ek<KK_NONE, NODEWISE>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_SE: return launch_ek<KK_SE, NODEWISE, SLM>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_DELTA: return launch_ek<KK_DELTA, NODEWISE, SLM>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    case KK_POLY: return launch_ek<KK_POLY, NODEWISE, SLM>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    default: return launch_ek<KK_NONE, NODEWISE, SLM>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
   }
 }
 
 cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue, int num_sms,
-                            cudaStream_t stream) {
-  if (out.nodewise) return launch_nw<true>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
-  return launch_nw<false>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+                            int slots, cudaStream_t stream) {
+  if (slots <= kNarrowSlots) {
+    if (out.nodewise) return launch_nw<true, kNarrowSlots>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+    return launch_nw<false, kNarrowSlots>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+  }
+  if (out.nodewise) return launch_nw<true, SLOTS>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
+  return launch_nw<false, SLOTS>(ds, vk, ek, job, prm, out, queue, num_sms, stream);
 }
 
 }  // namespace mgk

@@ -16,7 +16,8 @@ from typing import Optional
 import numpy as np
 
 from . import native
-from .basekernels import as_kernel, BaseKernel, ConstantOne, KroneckerDelta, SquareExponential, CompactPolynomial
+from .basekernels import (as_kernel, BaseKernel, CompactPolynomial, ConstantOne, KroneckerDelta, ProductComposite,
+                          RConvolution, SquareExponential)
 from .graphs import LabeledGraph, validate_graph
 
 DEFAULT_VERTEX_FLOOR = 1e-12
@@ -65,6 +66,8 @@ def kernel_spec(k: BaseKernel | None) -> str | None:
     if isinstance(k, CompactPolynomial):
         k.device_descriptor()  # raises for unsupported variants
         return "poly:" + ",".join(repr(c) for c in k.coeffs)
+    if isinstance(k, (ProductComposite, RConvolution)):
+        return k.spec()
     k.device_descriptor()
     raise NotImplementedError(f"{type(k).__name__} has no device lowering yet")
 

@@ -1,6 +1,6 @@
 """Generate golden vectors by running the REAL reference (build container only).
 
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [composite]
 
 The reference (``mgksolver``, /root/reference/pkg/src) is imported read-only
 and evaluated on seeded inputs; inputs and outputs are written to
@@ -226,7 +226,73 @@ def make_gram():
     }
 
 
+def ref_kernel(spec, role):
+    """Extended spec (prod:K1|K2, rconv:K) -> the reference's ProductComposite / RConvolution objects."""
+    if spec is None:
+        return None
+    head, _, rest = spec.partition(":")
+    if head == "prod":
+        k = ref.ProductComposite([ref.kernel_from_spec(p) for p in rest.split("|")])
+    elif head == "rconv":
+        k = ref.RConvolution(ref.kernel_from_spec(rest))
+    else:
+        k = ref.kernel_from_spec(spec)
+    return k.with_role(role)
+
+
+def composite_graph(rng, n, edge_dim, node_dim, density=0.3, w_range=(0.2, 2.0), q_range=(0.2, 0.9)):
+    """Vector-labelled graph: node labels small ints (element, charge); edge labels
+    (length, bond order) for edge_dim 2, three lengths for edge_dim 3."""
+    edges, el = [], []
+    for i in range(n):
+        for j in range(i + 1, n):
+            if rng.random() < density:
+                edges.append((i, j, float(rng.uniform(*w_range))))
+                d = float(rng.uniform(0.5, 2.0))
+                el.append([d, float(rng.integers(1, 4))] if edge_dim == 2 else
+                          [d, d * float(rng.uniform(0.5, 1.5)), float(rng.uniform(0.0, 2.0))])
+    nl = rng.integers(0, 3, size=(n, node_dim)).astype(float)
+    return ref.LabeledGraph.from_edges(n, edges, node_labels=nl, edge_labels=np.array(el) if edges else None,
+                                       start_prob=rng.uniform(0.1, 1.0, size=n),
+                                       stop_prob=rng.uniform(*q_range, size=n))
+
+
+def make_composite():
+    """ProductComposite / RConvolution pairs through the reference kernel() (composite.json)."""
+    rng = np.random.default_rng(175)
+    cases = []
+    for trial in range(4):
+        ga = composite_graph(rng, int(rng.integers(5, 22)), 2, 2)
+        gb = composite_graph(rng, int(rng.integers(5, 22)), 2, 2)
+        cases.append((f"prod{trial}", ga, gb, "prod:delta:0.5|delta:0.8", "prod:se:1.0|delta:0.5"))
+    # RConvolution values reach dim^2 (the kernel's range exceeds 1, basekernels.py:217-219): light
+    # weights and large q keep these product systems positive definite
+    for trial in range(3):
+        kw = dict(w_range=(0.05, 0.2), q_range=(0.5, 0.9))
+        ga = composite_graph(rng, int(rng.integers(5, 18)), 3, 2, **kw)
+        gb = composite_graph(rng, int(rng.integers(5, 18)), 3, 2, **kw)
+        cases.append((f"rconv{trial}", ga, gb, "delta:0.5", "rconv:se:0.7"))
+    kw = dict(w_range=(0.05, 0.2), q_range=(0.5, 0.9))
+    ga = composite_graph(rng, 12, 3, 1, **kw)
+    gb = composite_graph(rng, 15, 3, 1, **kw)
+    cases.append(("rconv_vertex", ga, gb, "rconv:delta:0.5", "rconv:se:0.7"))
+    ga = composite_graph(rng, 30, 2, 2, density=0.2)
+    gb = composite_graph(rng, 26, 2, 2, density=0.2)
+    cases.append(("prod_poly", ga, gb, "prod:const1|delta:0.5", "prod:poly:1.0,-0.3,0.02|se:0.5"))
+    out = []
+    for name, ga, gb, vs, es in cases:
+        res = ref.kernel(ga, gb, ref_kernel(vs, "vertex"), ref_kernel(es, "edge"))
+        out.append({"name": name, "a": gjson(ga), "b": gjson(gb), "vkernel": vs, "ekernel": es, "tol": 1e-10,
+                    "value": res.value, "iterations": res.iterations, "nodewise": res.nodewise.tolist()})
+        print("composite", name, res.iterations, flush=True)
+    return out
+
+
 def main():
+    if sys.argv[1:] == ["composite"]:
+        (HERE / "composite.json").write_text(json.dumps(make_composite()))
+        print("done")
+        return
     (HERE / "rng.json").write_text(json.dumps(make_rng_vectors(), indent=0))
     (HERE / "structure.json").write_text(json.dumps(make_structure()))
     (HERE / "kernels.json").write_text(json.dumps(make_kernels()))

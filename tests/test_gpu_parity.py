@@ -74,6 +74,20 @@ def test_kernel_golden_pairs(mgk, golden_kernels):
         assert np.max(np.abs(res.nodewise - nw)) <= REL * np.max(np.abs(nw)), rec["name"]
 
 
+def test_composite_kernels_golden(mgk):
+    """ProductComposite / RConvolution edge and vertex kernels (vector labels, evaluated in-kernel by the
+    generic CTA solver) against the reference kernel() values (tests/golden/composite.json)."""
+    from conftest import load_golden
+
+    for rec in load_golden("composite.json"):
+        ga, gb = graph_from_json(rec["a"]), graph_from_json(rec["b"])
+        k = mgk.kernel(ga, gb, rec["vkernel"], rec["ekernel"])
+        assert abs(k.value - rec["value"]) <= REL * abs(rec["value"]), (rec["name"], k.value, rec["value"])
+        assert abs(k.iterations - rec["iterations"]) <= 1, (rec["name"], k.iterations, rec["iterations"])
+        nw = np.asarray(rec["nodewise"])
+        assert np.max(np.abs(k.nodewise - nw)) <= REL * np.max(np.abs(nw)), rec["name"]
+
+
 def test_closed_forms(mgk):
     a = mgk.LabeledGraph.from_edges(1, [], node_labels=np.array([0]), stop_prob=[0.3], start_prob=[1.0])
     b = mgk.LabeledGraph.from_edges(1, [], node_labels=np.array([1]), stop_prob=[0.3], start_prob=[1.0])

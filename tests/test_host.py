@@ -46,7 +46,7 @@ def test_schedule_pairs_matches_reference(golden_gram):
 
 def test_kernel_spec_lowering():
     from paper_1910_06310_b200 import (CompactPolynomial, ConstantOne, KroneckerDelta, ProductComposite,
-                                       SquareExponential, kernel_from_spec)
+                                       RConvolution, SquareExponential, kernel_from_spec)
     from paper_1910_06310_b200.solver import kernel_spec
 
     assert kernel_spec(None) is None
@@ -55,8 +55,14 @@ def test_kernel_spec_lowering():
     assert kernel_spec(SquareExponential(1.25)) == "se:1.25"
     assert kernel_spec(CompactPolynomial([1.0, -0.5])) == "poly:1.0,-0.5"
     assert kernel_spec(kernel_from_spec("se:2.0")) == "se:2.0"
+    # composites lower to the extended grammar; nesting and >4 components have no device lowering
+    assert kernel_spec(ProductComposite([ConstantOne(), SquareExponential(0.5)])) == "prod:const1|se:0.5"
+    assert kernel_spec(RConvolution(KroneckerDelta(0.25))) == "rconv:delta:0.25"
+    assert kernel_spec(kernel_from_spec("prod:delta:0.5|poly:1.0,-0.2")) == "prod:delta:0.5|poly:1.0,-0.2"
     with pytest.raises(NotImplementedError):
-        kernel_spec(ProductComposite([ConstantOne()]))
+        kernel_spec(ProductComposite([RConvolution(ConstantOne())]))
+    with pytest.raises(NotImplementedError):
+        kernel_spec(ProductComposite([ConstantOne()] * 5))
     with pytest.raises(ValueError):
         KroneckerDelta(0.0)
     assert KroneckerDelta(0.5).flop_count == 1 and SquareExponential(1.0).flop_count == 4

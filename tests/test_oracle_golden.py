@@ -80,6 +80,19 @@ def test_kernel_values_iterations(golden_kernels):
         assert np.allclose(res.nodewise, np.asarray(rec["nodewise"]), rtol=1e-10, atol=1e-14), rec["name"]
 
 
+def test_composite_kernels_golden():
+    """ProductComposite / RConvolution (basekernels.py:175-244) restated in the oracle, pinned
+    against the reference kernel() on vector-labelled pairs (tests/golden/composite.json)."""
+    from conftest import load_golden
+
+    for rec in load_golden("composite.json"):
+        ga, gb = graph_from_json(rec["a"]), graph_from_json(rec["b"])
+        res = O.kernel(ga, gb, rec["vkernel"], rec["ekernel"], tol=rec["tol"])
+        assert res.iterations == rec["iterations"], rec["name"]
+        assert abs(res.value - rec["value"]) <= 1e-11 * abs(rec["value"]), rec["name"]
+        assert np.allclose(res.nodewise, np.asarray(rec["nodewise"]), rtol=1e-9, atol=1e-14), rec["name"]
+
+
 def test_closed_forms():
     # reference tests/test_solver.py:38-69
     from paper_1910_06310_b200.graphs import LabeledGraph
