@@ -86,6 +86,12 @@ int mgk_degrees(mgk_ctx* ctx, int32_t g, double* d_out);
  * device-resident benchmark).  max_iter 0 -> 10*n*m (solver.py:87). */
 int mgk_gram(mgk_ctx* ctx, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv);
 
+/* mgk_gram followed by normalize_gram (gram.py:98-107) on the device-resident
+ * matrix: K[a,b] / sqrt(K[a,a] K[b,b]), unit diagonal, NaN propagates; a
+ * non-NaN diagonal entry <= 0 fails with MGK_E_INVALID (the reference's
+ * ValueError).  Replaces mgkbind.gram(normalize=True) (__init__.py:70-92). */
+int mgk_gram_normalized(mgk_ctx* ctx, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv);
+
 /* Shard of the Gram pairs for multi-GPU runs (the per-GPU part of the
  * 8-GPU pair scheduling in north_star; the reference's equivalent is the
  * pair queue of gram.py:69-86): this context solves the pairs whose

@@ -981,6 +981,22 @@ int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters
   return MGK_OK;
 }
 
+int mgk_gram_normalized(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv) {
+  int rc = mgk_gram(c, tol, max_iter, nullptr, iters, conv);
+  if (rc) return rc;
+  const int64_t G = c->G;
+  DBuf<double> diag;
+  DBuf<int> bad;
+  CUDA_TRY(diag.alloc(G));
+  CUDA_TRY(bad.alloc(1));
+  bool nonpositive = false;
+  CUDA_TRY(launch_gram_normalize(c->d_K.ptr, G, diag.ptr, bad.ptr, c->num_sms, c->stream, &nonpositive));
+  if (nonpositive) return fail(MGK_E_INVALID, "Gram diagonal must be strictly positive");
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (K) CUDA_TRY(d2h(K, c->d_K.ptr, G * G * sizeof(double)));
+  return MGK_OK;
+}
+
 static int64_t shard_len(int64_t total, int rank, int world) {
   return total > rank ? (total - rank + world - 1) / world : 0;
 }

@@ -141,6 +141,9 @@ cudaError_t launch_pcg_grid(const DatasetDev& ds, const KernelDesc& vk, const Ke
                             const SolveParams& prm, const SolveOut& out, float* vec, int64_t vstride, double2* gbuf,
                             int nblocks, cudaStream_t stream);
 int grid_blocks(int num_sms);
+// Gram post-processing (gram_post.cu)
+cudaError_t launch_gram_normalize(double* K, int64_t G, double* diag, int* bad, int num_sms, cudaStream_t stream,
+                                  bool* nonpositive);
 cudaError_t launch_pcg_block(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                              const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                              float* scratch, int64_t scratch_floats_per_cta, int nctas, cudaStream_t stream);

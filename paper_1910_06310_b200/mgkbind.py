@@ -106,10 +106,10 @@ def gram(graphs: list[BoundGraph], *, normalize: bool = False, workers: int = 1,
     vk, ek, cfg, q, unl, _ = _opts(options)
     try:
         ds = [_to_graph(g, q, unl) for g in graphs]
-        res = compute_gram(ds, vk, ek, cfg, workers=workers, deterministic=deterministic)
+        res = compute_gram(ds, vk, ek, cfg, workers=workers, deterministic=deterministic, normalize=normalize)
     except ValueError as exc:
         if "dense adjacency" in str(exc):
             raise
         raise SolverError(str(exc)) from exc
-    m = normalize_gram(res.matrix) if normalize else res.matrix
+    m = res.matrix
     return m, ~np.isnan(m)

@@ -32,6 +32,7 @@ SIGNATURES = {
     "mgk_tiles": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P]),
     "mgk_degrees": (C.c_int, [_P, C.c_int32, _P]),
     "mgk_gram": (C.c_int, [_P, C.c_double, C.c_int64, _P, _P, _P]),
+    "mgk_gram_normalized": (C.c_int, [_P, C.c_double, C.c_int64, _P, _P, _P]),
     "mgk_gram_shard": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, _P, _P, _P, _P, _P, _P]),
     "mgk_pairs": (C.c_int, [_P, C.c_int64, _P, _P, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
     "mgk_kernel": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
@@ -155,6 +156,15 @@ class Context:
         it = np.empty((G, G), dtype=np.int32)
         cv = np.empty((G, G), dtype=np.uint8)
         check(self.lib.mgk_gram(self.h, float(tol), int(max_iter), _ptr(K), _ptr(it), _ptr(cv)))
+        return K, it, cv.astype(bool)
+
+    def gram_normalized(self, tol: float, max_iter: int = 0):
+        """Gram matrix normalised on the device (normalize_gram, gram.py:98-107)."""
+        G = self.G
+        K = np.empty((G, G), dtype=np.float64)
+        it = np.empty((G, G), dtype=np.int32)
+        cv = np.empty((G, G), dtype=np.uint8)
+        check(self.lib.mgk_gram_normalized(self.h, float(tol), int(max_iter), _ptr(K), _ptr(it), _ptr(cv)))
         return K, it, cv.astype(bool)
 
     def gram_shard(self, rank: int, world: int, tol: float, max_iter: int = 0):

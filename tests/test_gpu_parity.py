@@ -110,6 +110,18 @@ def test_gram_config1_golden(mgk, golden_gram):
     assert np.allclose(mgk.normalize_gram(res.matrix), np.asarray(rec["normalized"]), rtol=2 * REL)
 
 
+def test_gram_normalized_on_device(mgk, golden_gram):
+    """normalize_gram (gram.py:98-107) applied on the device == the host restatement == the golden matrix."""
+    rec = golden_gram["config1"]
+    graphs = [graph_from_json(g) for g in rec["graphs"]]
+    res = mgk.compute_gram(graphs, rec["vkernel"], rec["ekernel"], normalize=True)
+    raw = mgk.compute_gram(graphs, rec["vkernel"], rec["ekernel"])
+    assert np.array_equal(np.diagonal(res.matrix), np.ones(len(graphs)))
+    assert np.allclose(res.matrix, mgk.normalize_gram(raw.matrix), rtol=1e-15, atol=0)
+    gold = np.asarray(rec["normalized"])
+    assert np.max(np.abs(res.matrix - gold) / np.abs(gold)) <= 2 * REL
+
+
 def test_gram_unlabeled_golden(mgk, golden_gram):
     rec = golden_gram["unlabeled5"]
     graphs = [graph_from_json(g) for g in rec["graphs"]]
