@@ -260,6 +260,14 @@ def reorder_dataset(ds, device: int):
     return [apply_permutation(g, p) for g, p in zip(ds, perms)]
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg: str):
+    """Phase progress on stderr (the JSON line stays alone on stdout)."""
+    print(f"[bench +{time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -275,9 +283,12 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
     raw = buckets(cfg, args.count)
+    log(f"config {cfg.key}: {sum(len(b) for _, b in raw)} graphs synthesised")
     t_pre = time.perf_counter()
     bks = [(name, reorder_dataset(ds, local_rank) if cfg.reorder else ds) for name, ds in raw]
     reorder_s = time.perf_counter() - t_pre
+    if cfg.reorder:
+        log(f"device PBR + apply: {reorder_s:.1f} s")
     ctxs = []
     for _, ds in bks:
         ctx = native.Context(local_rank)
@@ -334,10 +345,11 @@ def run_ours(args, rank, world, local_rank):
             g_tot += t0.elapsed_time(t1)
         return ms_tot, nl_tot, g_tot
 
-    for _ in range(args.warmup):
+    for w in range(args.warmup):
         flush.zero_()
         barrier()
         step()
+        log(f"warmup {w + 1}/{args.warmup} done")
     solve_ms, gather_ms, launches = [], [], 0
     barrier()
     with ClockSampler(local_rank) as clocks:
@@ -349,6 +361,7 @@ def run_ours(args, rank, world, local_rank):
             solve_ms.append(ms)
             gather_ms.append(gms)
             launches += nl
+            log(f"timed step: solve {ms:.1f} ms, gather {gms:.1f} ms")
     per_step = np.array(solve_ms) + np.array(gather_ms)
     t_local = torch.tensor([float(np.mean(per_step)), float(np.mean(solve_ms))], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -386,6 +399,7 @@ def run_ours(args, rank, world, local_rank):
                 it_dev = max(it_dev, abs(int(it[x, y]) - o.iterations))
                 checked += 1
         del Ks
+        log(f"parity sample done ({checked} pairs)")
         fp32_peak, ex2_peak = ctxs[0].peaks(local_rank)
         achieved = flops / world / (ms_solve * 1e-3) / 1e12
         traffic, traffic_src = traffic_from_profiles(cfg)
@@ -410,6 +424,7 @@ def run_ours(args, rank, world, local_rank):
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         h1, d1 = ctxs[0].transfer_bytes()
         e2e_val = npairs / (float(np.mean(e2e_ms)) * 1e-3)
+        log(f"e2e done: {np.mean(e2e_ms):.1f} ms")
 
         # ---- CPU oracle baseline on this host
         cores = os.cpu_count() or 1
@@ -417,6 +432,7 @@ def run_ours(args, rank, world, local_rank):
         ncpu = args.cpu_pairs if args.cpu_pairs is not None else cfg.cpu_pairs
         if ncpu:
             cpu_rate, cpu_dt, _, _ = cpu_pairs_per_sec(cfg, bks, ncpu, 7, cores)
+            log(f"cpu baseline done: {cpu_rate:.1f} pairs/s")
             cpu = {
                 "value": cpu_rate,
                 "unit": "pairs/s",

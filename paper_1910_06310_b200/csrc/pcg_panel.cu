@@ -332,6 +332,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     {
       int rpc = (n * v.np) / (4 * kPW);
       rpc = rpc < 2 ? 2 : (rpc > 32 ? 32 : rpc);
+      if (prm.panel_rpc > 0) rpc = prm.panel_rpc;
       v.rpc = (rpc + 1) & ~1;
     }
 
@@ -645,7 +646,7 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     v.n = n;
     v.m = m;
     v.np = SL > 128 ? L.npanels : 1;
-    v.rpc = 8;
+    v.rpc = prm.panel_rpc > 0 ? ((prm.panel_rpc + 1) & ~1) : 8;
     const int64_t di = gthreads / m, dl = gthreads % m;
 
     double2 acc = make_double2(0.0, 0.0);
