@@ -304,10 +304,10 @@ struct mgk_ctx {
   DBuf<float> d_resid, d_scratch, d_nodewise, d_gridvec;
   DBuf<double2> d_gridbuf;
   DBuf<int64_t> d_nwoff;
-  DBuf<int32_t> d_pa, d_pb, d_rowcol, d_wide;
+  DBuf<int32_t> d_pa, d_pb, d_rowcol;
   DBuf<int64_t> d_rowpre;
   // host images of the Gram job lists (host-side pair decoding for streaming)
-  std::vector<int32_t> h_lists, h_rowcol, h_wide;
+  std::vector<int32_t> h_lists, h_rowcol;
   std::vector<int64_t> h_rowpre;
   // pinned staging for streamed nodewise chunks
   float* h_nw = nullptr;
@@ -701,9 +701,10 @@ static bool small_graph(const mgk_ctx* c, const GraphDesc& d) {
 }
 
 // n * m at or below which a small pair is solved by the FP64 tiny kernel
+// (clamped to 128: then min(n, m) <= 11 and the smaller graph fits the tiny kernel's 4 lane slots)
 static int tiny_nm() {
   const char* t = getenv("MGK_TINY_NM");
-  return t ? atoi(t) : 128;
+  return t ? std::max(0, std::min(128, atoi(t))) : 128;
 }
 
 static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
@@ -713,6 +714,7 @@ static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   p.v_min = 1e-12f;
   p.tiny_nm = tiny_nm();
   p.panel_rpc = getenv("MGK_PANEL_RPC") ? atoi(getenv("MGK_PANEL_RPC")) : 0;
+  p.tiny_mode = getenv("MGK_TINY_MODE") ? atoi(getenv("MGK_TINY_MODE")) : 0;
   // product.py:153-161 with dataset-uniform label presence; kappa = 1 when ek is None/const1
   p.labeled = (c->el_kind != LK_NONE && c->espec.kind != KK_NONE && c->espec.kind != KK_CONST1) ? 1 : 0;
   return p;
@@ -778,7 +780,8 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
       slabs[k] = 5 * ((nm + 31) / 32 * 32);
       // P and Ap in shared memory when every pair of the job fits; else all pairs keep them in HBM/L2
       // and the whole L1 stays available to the gathers
-      svec[k] = nm <= kPanelSmemNM ? (int)(2 * nm) : 0;
+      const int64_t smem_nm = getenv("MGK_PANEL_SMEM_NM") ? atoll(getenv("MGK_PANEL_SMEM_NM")) : kPanelSmemNM;
+      svec[k] = nm <= smem_nm ? (int)(2 * nm) : 0;
       int per_sm = panel_ctas_per_sm(svec[k]);
       if (const char* e = getenv("MGK_PANEL_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
       ctas[k] = per_sm * c->num_sms;
@@ -861,21 +864,35 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
     if (x.ne != y.ne) return x.ne > y.ne;
     return a < b;
   };
-  std::stable_sort(small.begin(), small.end(), by_size);
+  // small list = [wide graphs (> 32 * kNarrowSlots nonzeros)] ++ [narrow graphs], each size-sorted:
+  // wide x wide pairs form the triangle of the prefix (wide warp instantiation); every other small
+  // pair has a narrow graph for the lane side (narrow instantiation)
+  auto is_wide = [c](int32_t g) { return (2 * c->graphs[g].ne + 31) / 32 > kNarrowSlots; };
+  std::stable_partition(small.begin(), small.end(), is_wide);
+  const int64_t P = std::count_if(small.begin(), small.end(), is_wide);
+  std::stable_sort(small.begin(), small.begin() + P, by_size);
+  std::stable_sort(small.begin() + P, small.end(), by_size);
   std::stable_sort(mid.begin(), mid.end(), by_size);
   std::stable_sort(large.begin(), large.end(), by_size);
   const int64_t ns = (int64_t)small.size(), nmid = (int64_t)mid.size(), nl = (int64_t)large.size();
   const int T = tiny_nm();
-  // ragged rows over the size-sorted small list
+  // ragged rows over the small list: row u pairs with columns [start(u), split(u)) on the narrow
+  // warp kernel and [split(u), ns) on the FP64 tiny kernel; start(u) = P for wide rows (their
+  // wide partners are in the prefix triangle), u otherwise.  Wide graphs are never tiny
+  // (S > 128 needs n >= 12), so tiny columns are a suffix of the n-sorted narrow part.
   std::vector<int64_t> mpre(ns + 1, 0), tpre(ns + 1, 0);
   std::vector<int32_t> mcol(ns), tcol(ns);
-  int64_t v = 0;
   for (int64_t u = 0; u < ns; ++u) {
     const int64_t nu = c->graphs[small[u]].n;
-    while (v < ns && (int64_t)c->graphs[small[v]].n * nu > T) ++v;
-    const int64_t split = std::max<int64_t>(u, v);
-    mcol[u] = (int32_t)u;
-    mpre[u + 1] = mpre[u] + (split - u);
+    const int64_t start = u < P ? P : u;
+    int64_t lo = std::max<int64_t>(start, P), hi = ns;  // first narrow column with n_u * n_v <= T
+    while (lo < hi) {
+      const int64_t mid_ = (lo + hi) / 2;
+      if ((int64_t)c->graphs[small[mid_]].n * nu > T) lo = mid_ + 1; else hi = mid_;
+    }
+    const int64_t split = std::max<int64_t>(start, lo);
+    mcol[u] = (int32_t)start;
+    mpre[u + 1] = mpre[u] + (split - start);
     tcol[u] = (int32_t)split;
     tpre[u + 1] = tpre[u] + (ns - split);
   }
@@ -924,23 +941,8 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
     return j;
   };
   const int cta = panel ? JK_PANEL : JK_BLOCK;
-  // pairs of two wide small graphs (> 32 * kNarrowSlots nonzeros each) leave the narrow warp
-  // instantiation (it skips them) for an explicit list on the wide one
-  std::vector<int32_t> wide;
-  for (int32_t g : small)
-    if ((2 * c->graphs[g].ne + 31) / 32 > kNarrowSlots) wide.push_back(g);
-  std::sort(wide.begin(), wide.end());
-  std::vector<int32_t> wl;
-  for (size_t x = 0; x < wide.size(); ++x)
-    for (size_t y = x; y < wide.size(); ++y) wl.push_back(wide[x]);
-  for (size_t x = 0; x < wide.size(); ++x)
-    for (size_t y = x; y < wide.size(); ++y) wl.push_back(wide[y]);
-  const int64_t nwide = (int64_t)wl.size() / 2;
-  CUDA_TRY(c->d_wide.upload(wl, s));
-  c->h_wide = wl;
-  JobSpec jw{};
-  jw.job = PairJob{PM_LIST, 0, 0, nwide, 0, 1, c->d_wide.ptr, c->d_wide.ptr + nwide, nullptr, nullptr};
-  jw.kernel = JK_WARP;
+  std::vector<int32_t> wide(small.begin(), small.begin() + P);
+  JobSpec jw = tri(wide, dsmall, JK_WARP);
   jw.slots = SmallClass::SLOTS;
   JobSpec jm{};
   jm.job = PairJob{PM_RAGGED, (int32_t)ns, 0, mpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr, c->d_rowcol.ptr};
@@ -1051,9 +1053,8 @@ static PairJob host_job(const mgk_ctx* c, const PairJob& j) {
   auto rebase32 = [&](const int32_t* p, const DBuf<int32_t>& d, const std::vector<int32_t>& hv) -> const int32_t* {
     return p ? hv.data() + (p - d.ptr) : nullptr;
   };
-  const bool wide = j.list_a && j.list_a >= c->d_wide.ptr && j.list_a < c->d_wide.ptr + c->d_wide.n;
-  h.list_a = wide ? rebase32(j.list_a, c->d_wide, c->h_wide) : rebase32(j.list_a, c->d_list_a, c->h_lists);
-  h.list_b = wide ? rebase32(j.list_b, c->d_wide, c->h_wide) : rebase32(j.list_b, c->d_list_a, c->h_lists);
+  h.list_a = rebase32(j.list_a, c->d_list_a, c->h_lists);
+  h.list_b = rebase32(j.list_b, c->d_list_a, c->h_lists);
   h.row_col0 = rebase32(j.row_col0, c->d_rowcol, c->h_rowcol);
   h.row_prefix = j.row_prefix ? c->h_rowpre.data() + (j.row_prefix - c->d_rowpre.ptr) : nullptr;
   return h;

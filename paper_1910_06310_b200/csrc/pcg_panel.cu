@@ -32,7 +32,10 @@ namespace mgk {
 
 namespace cg = cooperative_groups;
 
-constexpr int kPT = 256;          // threads per CTA
+#ifndef MGK_PANEL_THREADS
+#define MGK_PANEL_THREADS 256
+#endif
+constexpr int kPT = MGK_PANEL_THREADS;  // threads per CTA
 constexpr int kPW = kPT / 32;     // warps per CTA
 constexpr int kSegFloats = 2 * kPanelCap;  // per-warp segment buffer (two U rows)
 constexpr int kPanelStaticSmem = kPW * kSegFloats * 4;
@@ -290,7 +293,7 @@ __device__ __forceinline__ int64_t lane_cost(const GraphDesc& g) {
 }
 
 template <int EK, bool NODEWISE>
-__global__ void __launch_bounds__(kPT, 2)
+__global__ void __launch_bounds__(kPT, 512 / kPT)
 k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
             unsigned long long* queue, float* scratch, int64_t slab, int smem_vec) {
   extern __shared__ __align__(16) float psm[];
@@ -600,7 +603,7 @@ __device__ double2 grid_sum2(double2 v, double2* gbuf, double2* wred, double2* s
 }
 
 template <int EK, bool NODEWISE>
-__global__ void __launch_bounds__(kPT, 2)
+__global__ void __launch_bounds__(kPT, 512 / kPT)
 k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out, float* vec,
            int64_t vstride, double2* gbuf) {
   cg::grid_group grid = cg::this_grid();

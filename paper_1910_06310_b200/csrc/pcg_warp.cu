@@ -156,8 +156,9 @@ template <int EK>
 __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
                            const GraphDesc& U, const GraphDesc& L, const float2* uwl, const int* uoff,
                            const int* urow, const float4* le, const int* lrow, double* P, double* AP, double* DG,
-                           int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw,
-                           bool swap) {
+                           float* PF, int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out,
+                           float* nw, bool swap) {
+  const bool fmv = prm.tiny_mode == 1;  // FP32 matvec on a float shadow of P (experiment switch)
   const int nu = U.n, m = L.n, nm = nu * m;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
   double r[4], x[4];
@@ -185,6 +186,7 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       r[s] = b;
       const double z = b / dg;
       P[e] = z;
+      PF[e] = (float)z;
       rho += b * z;
       rr += b * b;
     }
@@ -203,13 +205,26 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       if (e < nm) {
         const int i = e / m, l = e - i * m;
         double acc = 0.0;
-        for (int k = urow[i]; k < urow[i + 1]; ++k) {
-          const float2 a = uwl[k];
-          const double* prow = P + (uoff[k] >> 7) * m;
-          for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
-            const float4 b = le[q];
-            const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
-            acc = fma((double)c, prow[__float_as_int(b.x)], acc);
+        if (fmv) {
+          float accf = 0.0f;
+          for (int k = urow[i]; k < urow[i + 1]; ++k) {
+            const float2 a = uwl[k];
+            const float* prow = PF + (uoff[k] >> 7) * m;
+            for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
+              const float4 b = le[q];
+              accf = fmaf(edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y, prow[__float_as_int(b.x)], accf);
+            }
+          }
+          acc = accf;
+        } else {
+          for (int k = urow[i]; k < urow[i + 1]; ++k) {
+            const float2 a = uwl[k];
+            const double* prow = P + (uoff[k] >> 7) * m;
+            for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
+              const float4 b = le[q];
+              const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
+              acc = fma((double)c, prow[__float_as_int(b.x)], acc);
+            }
           }
         }
         AP[e] = DG[e] * P[e] - acc;
@@ -246,7 +261,10 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
-      if (e < nm) P[e] = r[s] / DG[e] + beta * P[e];
+      if (e < nm) {
+        P[e] = r[s] / DG[e] + beta * P[e];
+        PF[e] = (float)P[e];
+      }
     }
     rho = rho_next;
     __syncwarp();
@@ -396,9 +414,10 @@ __device__ __forceinline__ void xmv_dispatch(int ns, Smem& S, const KernelDesc& 
 }
 
 // SLM: lane-side slot capacity of this instantiation.  SLM = 4 (S_L <= 128)
-// covers ~95% of QM7-shaped pairs with a third of the registers; it skips the
-// pairs whose graphs both exceed 128 nonzeros, which the host routes to the
-// SLM = 10 instantiation as an explicit list.
+// covers ~95% of QM7-shaped pairs with a third of the registers; the host
+// routes the pairs whose graphs both exceed 128 nonzeros to the SLM = 10
+// instantiation (gram_jobs: the wide-prefix triangle), so every pair of a
+// narrow job has a narrow graph for the lane side.
 template <int EK, bool NODEWISE, int SLM>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, SLM <= 4 ? 8 : 6)
 k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
@@ -429,7 +448,7 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     bool swap = (costBA < costAB);
     if (SLM < SLOTS) {
       if ((swap ? nsA : nsB) > SLM) swap = !swap;
-      if ((swap ? nsA : nsB) > SLM) continue;  // both graphs too wide: the SLM = 10 list has this pair
+      if ((swap ? nsA : nsB) > SLM) continue;  // not routed here by the host (both graphs wide)
     }
     const GraphDesc U = swap ? B : A;
     const GraphDesc L = swap ? A : B;
@@ -601,6 +620,7 @@ struct TinySmem {
   int UOFF[SMAX];
   float4 LE[SMAX];
   double V[3 * kTinyMax];  // P, AP, DG
+  float PF[kTinyMax];      // float shadow of P (tiny_mode 1)
   int urow[NU + 8];
   int lrow[40];
 };
@@ -634,7 +654,7 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     bool conv;
     float* nw = out.nodewise ? out.nodewise + out.nodewise_off[pid] : nullptr;
     solve_tiny<EK>(ds, vk, ek, prm, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.V, S.V + kTinyMax,
-                   S.V + 2 * kTinyMax, lane, val, it, conv, rr, nw, false);
+                   S.V + 2 * kTinyMax, S.PF, lane, val, it, conv, rr, nw, false);
     write_pair_outputs(out, pid, ga, gb, val, it, conv, rr, lane);
     __syncwarp();
   }
