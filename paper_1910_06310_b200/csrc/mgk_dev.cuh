@@ -101,6 +101,27 @@ __device__ __forceinline__ float edge_kappa(const KernelDesc& k, float a, float 
   }
 }
 
+// kappa(a, b) * w with the weight carried in the form the kind prefers: for SE
+// the U-side weight is stored as log2(w) and folded into the exponent,
+// kappa * w = exp2(log2 w - (a - b)^2)  (FADD + FFMA + MUFU.EX2 per contribution);
+// the other kinds multiply (wf = w).
+template <int EK>
+__device__ __forceinline__ float edge_kappa_w(const KernelDesc& k, float a, float b, float wf) {
+  if constexpr (EK == KK_SE) {
+    const float d = a - b;
+    return ex2_approx(fmaf(-d, d, wf));
+  } else {
+    return edge_kappa<EK>(k, a, b) * wf;
+  }
+}
+
+// U-side weight in the form edge_kappa_w expects.
+template <int EK>
+__device__ __forceinline__ float weight_form(float w) {
+  if constexpr (EK == KK_SE) return log2f(w);
+  return w;
+}
+
 // Label storage kinds (graphs.py:126-146).
 enum LabelKind : int32_t { LK_NONE = 0, LK_CAT = 1, LK_VEC = 2 };
 

@@ -102,8 +102,8 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
     const float4 g0 = entry(k + 4), g1 = entry(k + 5);
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
-      acc[t] = fmaf(edge_kappa<EK>(ek, e0.z, llab[t]), e0.y * p0[t], acc[t]);
-      acc[t] = fmaf(edge_kappa<EK>(ek, e1.z, llab[t]), e1.y * p1[t], acc[t]);
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y), p0[t], acc[t]);
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e1.z, llab[t], EK == KK_SE ? e1.w : e1.y), p1[t], acc[t]);
     }
     e0 = f0;
     e1 = f1;
@@ -136,15 +136,16 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
     }
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
-      acc[t] = fmaf(edge_kappa<EK>(ek, e0.z, llab[t]), e0.y * p0[t], acc[t]);
-      acc[t] = fmaf(edge_kappa<EK>(ek, e1.z, llab[t]), e1.y * p1[t], acc[t]);
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y), p0[t], acc[t]);
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e1.z, llab[t], EK == KK_SE ? e1.w : e1.y), p1[t], acc[t]);
     }
   }
   if (k < k1) {
     const float4 e0 = ue[k];
     const float* r0 = P + __float_as_int(e0.x) * m;
 #pragma unroll
-    for (int t = 0; t < NS; ++t) acc[t] = fmaf(edge_kappa<EK>(ek, e0.z, llab[t]), e0.y * r0[lcol[t]], acc[t]);
+    for (int t = 0; t < NS; ++t)
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y), r0[lcol[t]], acc[t]);
   }
 }
 

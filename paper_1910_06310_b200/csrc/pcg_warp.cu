@@ -50,8 +50,7 @@ struct WarpSmem {
   float OFF[NU][32];
   float T[UNLAB ? NU : 1][32];
   float X[NODEWISE ? NU : 1][32];
-  float2 UWL[SMAX];       // U nonzeros in row order: {w, label}
-  int UOFF[SMAX];         //   and the byte offset of P row j (j * 128)
+  float4 UE[SMAX];        // U nonzeros in row order: {weight form, label, byte offset of P row j, -}
   float SEG[2 * 32 * SLM];  // segment sums of two U-rows
   int urow[NU + 8];
   int lrow[40];
@@ -296,9 +295,9 @@ __device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& 
   const int k1 = S.urow[i + 1];
   int k = S.urow[i];
   for (; k + 1 < k1; k += 2) {
-    const float2 e0 = S.UWL[k], e1 = S.UWL[k + 1];
-    const char* r0 = pbase + S.UOFF[k];
-    const char* r1 = pbase + S.UOFF[k + 1];
+    const float4 e0 = S.UE[k], e1 = S.UE[k + 1];
+    const char* r0 = pbase + __float_as_int(e0.z);
+    const char* r1 = pbase + __float_as_int(e1.z);
     float p0[NS], p1[NS];
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
@@ -307,16 +306,16 @@ __device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& 
     }
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
-      acc[t] = fmaf(edge_kappa<EK>(ek, e0.y, llab[t]), e0.x * p0[t], acc[t]);
-      acc[t] = fmaf(edge_kappa<EK>(ek, e1.y, llab[t]), e1.x * p1[t], acc[t]);
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), p0[t], acc[t]);
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e1.y, llab[t], e1.x), p1[t], acc[t]);
     }
   }
   if (k < k1) {
-    const float2 e0 = S.UWL[k];
-    const char* r0 = pbase + S.UOFF[k];
+    const float4 e0 = S.UE[k];
+    const char* r0 = pbase + __float_as_int(e0.z);
 #pragma unroll
     for (int t = 0; t < NS; ++t)
-      acc[t] = fmaf(edge_kappa<EK>(ek, e0.y, llab[t]), e0.x * *reinterpret_cast<const float*>(r0 + lcoff[t]),
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), *reinterpret_cast<const float*>(r0 + lcoff[t]),
                     acc[t]);
   }
 }
@@ -375,7 +374,10 @@ __device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, 
   }
   for (int i = 0; i < nu; ++i) {
     float s = 0.0f;
-    for (int k = S.urow[i]; k < S.urow[i + 1]; ++k) s = fmaf(S.UWL[k].x, S.T[S.UOFF[k] >> 7][lane], s);
+    for (int k = S.urow[i]; k < S.urow[i + 1]; ++k) {
+      const float4 e = S.UE[k];
+      s = fmaf(e.x, S.T[__float_as_int(e.z) >> 7][lane], s);
+    }
     if (lane < m) S.OFF[i][lane] = s;
   }
   __syncwarp();
@@ -456,10 +458,9 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     const int SL = 2 * L.ne;
     const int ns = (SL + 31) >> 5;
 
-    // ---- prologue: octiles -> rows (U into UWL/UOFF, L staged then held in registers)
+    // ---- prologue: octiles -> rows (U into UE, L staged then held in registers)
     octiles_to_rows(ds, U, lane, S.urow, el_dim, [&](int pos, int col, float w, float lab) {
-      S.UWL[pos] = make_float2(w, lab);
-      S.UOFF[pos] = col * 128;
+      S.UE[pos] = make_float4(weight_form<EK>(w), lab, __int_as_float(col * 128), 0.0f);
     });
     octiles_to_rows(ds, L, lane, S.lrow, el_dim, [&](int pos, int col, float w, float lab) {
       stage[pos] = make_float4(__int_as_float(col), w, lab, 0.0f);

@@ -224,7 +224,7 @@ __global__ void k_trow(int G, const int64_t* __restrict__ gseg, const int64_t* _
 
 // Row-ordered expansion of the octiles for the panel solver: node i's nonzeros
 // (ascending column, the order its tile row implies) land at
-// rowent[nz_off + rowptr[i] ..].  Thread per node.
+// rowent[nz_off + rowptr[i] ..] as {col, w, label, log2 w}.  Thread per node.
 __global__ void k_rows_fill(int64_t ntotal, const int32_t* __restrict__ node_graph, const GraphDesc* __restrict__ graphs,
                             const Octile* __restrict__ tiles, const int32_t* __restrict__ trow,
                             const float* __restrict__ nz_w, const float* __restrict__ nz_label, int el_dim,
@@ -244,7 +244,7 @@ __global__ void k_rows_fill(int64_t ntotal, const int32_t* __restrict__ node_gra
     for (int c = 0; byte; ++c, byte &= byte - 1) {
       const int64_t k = base + c;
       const float lab = el_dim > 0 ? nz_label[k * el_dim] : 0.0f;
-      dst[pos++] = make_float4(__int_as_float(o.col * 8 + (__ffs(byte) - 1)), nz_w[k], lab, 0.0f);
+      dst[pos++] = make_float4(__int_as_float(o.col * 8 + (__ffs(byte) - 1)), nz_w[k], lab, log2f(nz_w[k]));
     }
   }
 }
