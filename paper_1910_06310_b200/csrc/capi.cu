@@ -714,7 +714,6 @@ static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   p.v_min = 1e-12f;
   p.tiny_nm = tiny_nm();
   p.panel_rpc = getenv("MGK_PANEL_RPC") ? atoi(getenv("MGK_PANEL_RPC")) : 0;
-  p.tiny_mode = getenv("MGK_TINY_MODE") ? atoi(getenv("MGK_TINY_MODE")) : 0;
   // product.py:153-161 with dataset-uniform label presence; kappa = 1 when ek is None/const1
   p.labeled = (c->el_kind != LK_NONE && c->espec.kind != KK_NONE && c->espec.kind != KK_CONST1) ? 1 : 0;
   return p;

@@ -51,7 +51,6 @@ struct SolveParams {
   int32_t labeled;          // edge mode decided per dataset (product.py:153-161)
   int32_t tiny_nm;          // n*m at or below which the warp solver runs the pair in FP64
   int32_t panel_rpc;        // U rows per panel work item (0: automatic)
-  int32_t tiny_mode;        // 0: FP64 matvec in the tiny solver, 1: FP32 matvec (experiment)
 };
 
 // Gram modes report a <= b (the reference's pair order, gram.py:38-54); lists keep the caller's order.

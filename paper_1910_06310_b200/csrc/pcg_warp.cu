@@ -154,13 +154,14 @@ constexpr int kTinyMax = 128;
 template <int EK>
 __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
                            const GraphDesc& U, const GraphDesc& L, const float2* uwl, const int* uoff,
-                           const int* urow, const float4* le, const int* lrow, double* P, double* AP, double* DG,
-                           float* PF, int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out,
-                           float* nw, bool swap) {
-  const bool fmv = prm.tiny_mode == 1;  // FP32 matvec on a float shadow of P (experiment switch)
+                           const int* urow, const float4* le, const int* lrow, double* P, int lane,
+                           double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw, bool swap) {
   const int nu = U.n, m = L.n, nm = nu * m;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
-  double r[4], x[4];
+  // the lane's elements e = lane + 32 s (s < 4) are private: residual, iterate, A p, the
+  // diagonal and its inverse stay in registers; only the direction P is shared (gathered)
+  double r[4], x[4], ap[4], dg[4], idg[4];
+  int ei[4], k0[4], k1[4], q0[4], q1[4];
   double bb_u = 0.0, bb_l = 0.0;
   if (lane < nu) {
     double dq = ds.deg[U.node_off + lane] * (double)ds.q[U.node_off + lane];
@@ -176,16 +177,25 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
     const int e = lane + 32 * s;
     r[s] = 0.0;
     x[s] = 0.0;
+    ap[s] = 0.0;
+    dg[s] = 1.0;
+    idg[s] = 1.0;
+    ei[s] = 0;
+    k0[s] = k1[s] = q0[s] = q1[s] = 0;
     if (e < nm) {
       const int i = e / m, l = e - i * m;
+      ei[s] = i;
+      k0[s] = urow[i];
+      k1[s] = urow[i + 1];
+      q0[s] = lrow[l];
+      q1[s] = lrow[l + 1];
       const int64_t vu = U.node_off + i, vl = L.node_off + l;
-      const double dg = diag_of(ds, vk, prm, vlab, vu, vl);
+      dg[s] = diag_of(ds, vk, prm, vlab, vu, vl);
+      idg[s] = 1.0 / dg[s];
       const double b = (ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]);
-      DG[e] = dg;
       r[s] = b;
-      const double z = b / dg;
+      const double z = b * idg[s];
       P[e] = z;
-      PF[e] = (float)z;
       rho += b * z;
       rr += b * b;
     }
@@ -198,45 +208,27 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
   int64_t it = 0;
   __syncwarp();
   while (!conv && it < max_iter) {
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int e = lane + 32 * s;
-      if (e < nm) {
-        const int i = e / m, l = e - i * m;
-        double acc = 0.0;
-        if (fmv) {
-          float accf = 0.0f;
-          for (int k = urow[i]; k < urow[i + 1]; ++k) {
-            const float2 a = uwl[k];
-            const float* prow = PF + (uoff[k] >> 7) * m;
-            for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
-              const float4 b = le[q];
-              accf = fmaf(edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y, prow[__float_as_int(b.x)], accf);
-            }
-          }
-          acc = accf;
-        } else {
-          for (int k = urow[i]; k < urow[i + 1]; ++k) {
-            const float2 a = uwl[k];
-            const double* prow = P + (uoff[k] >> 7) * m;
-            for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
-              const float4 b = le[q];
-              const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
-              acc = fma((double)c, prow[__float_as_int(b.x)], acc);
-            }
-          }
-        }
-        AP[e] = DG[e] * P[e] - acc;
-      }
-    }
-    __syncwarp();
-    ++it;
     double pap = 0.0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
-      if (e < nm) pap += P[e] * AP[e];
+      if (e < nm) {
+        double acc = 0.0;
+        for (int k = k0[s]; k < k1[s]; ++k) {
+          const float2 a = uwl[k];
+          const double* prow = P + (uoff[k] >> 7) * m;
+          for (int q = q0[s]; q < q1[s]; ++q) {
+            const float4 b = le[q];
+            const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
+            acc = fma((double)c, prow[__float_as_int(b.x)], acc);
+          }
+        }
+        const double p = P[e];
+        ap[s] = dg[s] * p - acc;
+        pap += p * ap[s];
+      }
     }
+    ++it;
     const double alpha = rho / warp_sum(pap);
     double rr_l = 0.0, rz_l = 0.0;
 #pragma unroll
@@ -244,9 +236,9 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       const int e = lane + 32 * s;
       if (e < nm) {
         x[s] += alpha * P[e];
-        r[s] -= alpha * AP[e];
+        r[s] -= alpha * ap[s];
         rr_l += r[s] * r[s];
-        rz_l += r[s] * (r[s] / DG[e]);
+        rz_l += r[s] * (r[s] * idg[s]);
       }
     }
     rr = warp_sum(rr_l);
@@ -256,14 +248,11 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       break;
     }
     const double beta = rho_next / rho;
-    __syncwarp();
+    __syncwarp();  // every lane has finished gathering P
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
-      if (e < nm) {
-        P[e] = r[s] / DG[e] + beta * P[e];
-        PF[e] = (float)P[e];
-      }
+      if (e < nm) P[e] = r[s] * idg[s] + beta * P[e];
     }
     rho = rho_next;
     __syncwarp();
@@ -620,8 +609,7 @@ struct TinySmem {
   float2 UWL[SMAX];
   int UOFF[SMAX];
   float4 LE[SMAX];
-  double V[3 * kTinyMax];  // P, AP, DG
-  float PF[kTinyMax];      // float shadow of P (tiny_mode 1)
+  double P[kTinyMax];      // PCG direction (the only shared vector)
   int urow[NU + 8];
   int lrow[40];
 };
@@ -654,8 +642,8 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int64_t it;
     bool conv;
     float* nw = out.nodewise ? out.nodewise + out.nodewise_off[pid] : nullptr;
-    solve_tiny<EK>(ds, vk, ek, prm, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.V, S.V + kTinyMax,
-                   S.V + 2 * kTinyMax, S.PF, lane, val, it, conv, rr, nw, false);
+    solve_tiny<EK>(ds, vk, ek, prm, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.P, lane, val, it, conv, rr, nw,
+                   false);
     write_pair_outputs(out, pid, ga, gb, val, it, conv, rr, lane);
     __syncwarp();
   }

@@ -39,11 +39,10 @@ if __name__ == "__main__":
     with mp.get_context("fork").Pool(os.cpu_count()) as pool:
         ref = np.array(pool.map(oracle, pairs, chunksize=64))
     n = np.array([g.node_count for g in DS])
-    modes = [(t, os.environ.get("MGK_TINY_MODE", "0")) for t in (0, 64, 128)]
-    for tiny, mode in modes:
+    for tiny in (0, 64, 128):
         it = device(tiny)
         d = np.array([int(it[a, b]) for a, b in pairs]) - ref
         bad = np.abs(d) > 1
         nm = np.array([n[a] * n[b] for a, b in pairs])
-        print(f"MGK_TINY_MODE={mode} MGK_TINY_NM={tiny}: {len(pairs)} pairs, |d_iter|>1: {bad.sum()}, nm of those: "
+        print(f"MGK_TINY_NM={tiny}: {len(pairs)} pairs, |d_iter|>1: {bad.sum()}, nm of those: "
               f"{sorted(set(nm[bad].tolist()))[:20]}, diff hist {np.unique(d, return_counts=True)}", flush=True)
