@@ -266,7 +266,8 @@ struct mgk_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t side[2] = {nullptr, nullptr};   // warp-class jobs run beside the CTA/grid jobs
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evside[2] = {nullptr, nullptr};
   double last_ms = 0.0;
   int last_launches = 0;
   // host copy of the dataset
@@ -335,6 +336,10 @@ int mgk_ctx_create(mgk_ctx** out, int device) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreate(&c->ev0));
   CUDA_TRY(cudaEventCreate(&c->ev1));
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->side[k], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->evside[k], cudaEventDisableTiming));
+  }
   *out = c;
   return MGK_OK;
 }
@@ -345,6 +350,11 @@ int mgk_ctx_destroy(mgk_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->side[k]) cudaStreamSynchronize(ctx->side[k]);
+    if (ctx->side[k]) cudaStreamDestroy(ctx->side[k]);
+    if (ctx->evside[k]) cudaEventDestroy(ctx->evside[k]);
+  }
   if (ctx->h_nw) cudaFreeHost(ctx->h_nw);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -802,7 +812,25 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   }
   c->last_launches = 0;
   CUDA_TRY(cudaEventRecord(c->ev0, s));
-  for (size_t k = 0; k < jobs.size(); ++k) {
+  // Streams: grid and CTA-class jobs in order on the main stream (they share the scratch slabs and the
+  // cooperative grid must own the device); warp-class jobs on side stream 0, tiny jobs on side stream
+  // 1.  Persistent kernels leave the device as their queues drain, so the concurrent jobs fill each
+  // other's tails.  MGK_SERIAL=1 runs everything on the main stream.
+  // The cooperative grid jobs go first and alone (their blocks must all be resident).
+  const bool serial = getenv("MGK_SERIAL") != nullptr;
+  bool used[2] = {false, false};
+  std::vector<size_t> order;
+  for (size_t k = 0; k < jobs.size(); ++k)
+    if (jobs[k].kernel == JK_GRID) order.push_back(k);
+  const size_t ngrid = order.size();
+  for (size_t k = 0; k < jobs.size(); ++k)
+    if (jobs[k].kernel != JK_GRID) order.push_back(k);
+  for (size_t oi = 0; oi < order.size(); ++oi) {
+    const size_t k = order[oi];
+    if (oi == ngrid) {
+      CUDA_TRY(cudaEventRecord(c->evside[0], s));
+      for (int q = 0; q < 2; ++q) CUDA_TRY(cudaStreamWaitEvent(c->side[q], c->evside[0], 0));
+    }
     JobSpec& j = jobs[k];
     if (j.job.npairs <= 0) continue;
     SolveOut o = out_base;
@@ -815,10 +843,13 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     if (o.pair_a) o.pair_a += off;
     if (o.pair_b) o.pair_b += off;
     cudaError_t e;
+    const int q = serial ? -1 : (j.kernel == JK_WARP ? 0 : (j.kernel == JK_TINY ? 1 : -1));
+    cudaStream_t js = q < 0 ? s : c->side[q];
+    if (q >= 0) used[q] = true;
     if (j.kernel == JK_WARP)
-      e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, j.slots, s);
+      e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, j.slots, js);
     else if (j.kernel == JK_TINY)
-      e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, s);
+      e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, js);
     else if (j.kernel == JK_GRID)
       e = launch_pcg_grid(c->ds, c->vk, c->ek, j.job, prm, o, c->d_gridvec.ptr, grid_vstride, c->d_gridbuf.ptr,
                           gblocks, s);
@@ -831,6 +862,15 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     if (e != cudaSuccess) return fail(MGK_E_CUDA, "solver launch failed: %s", cudaGetErrorString(e));
     ++c->last_launches;
   }
+  if (ngrid == order.size()) {  // only grid jobs (or none): the side streams still join below
+    CUDA_TRY(cudaEventRecord(c->evside[0], s));
+    for (int q = 0; q < 2; ++q) CUDA_TRY(cudaStreamWaitEvent(c->side[q], c->evside[0], 0));
+  }
+  for (int q = 0; q < 2; ++q) {
+    CUDA_TRY(cudaEventRecord(c->evside[q], c->side[q]));
+    CUDA_TRY(cudaStreamWaitEvent(s, c->evside[q], 0));
+  }
+  (void)used;
   CUDA_TRY(cudaEventRecord(c->ev1, s));
   CUDA_TRY(cudaEventSynchronize(c->ev1));
   CUDA_TRY(cudaGetLastError());
