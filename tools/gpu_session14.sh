@@ -4,9 +4,9 @@ timeout 300 python tools/prof_gram.py 7165 3 2>&1 | tail -1
 MGK_SERIAL=1 timeout 300 python tools/prof_gram.py 7165 3 2>&1 | tail -1
 timeout 300 python tools/prof_c5.py 3000 2>&1 | tail -1
 MGK_SERIAL=1 timeout 300 python tools/prof_c5.py 3000 2>&1 | tail -1
-timeout 600 MGK_SERIAL=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/prof_gram.py 7165 1 > /dev/null 2>&1
+MGK_SERIAL=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/prof_gram.py 7165 1 > /dev/null 2>&1
 grep -E "k_pcg" gpurun_out/launches_c2.csv | awk -F'","' '{print $5, $(NF)}' | cut -c1-150
 timeout 1100 python tools/tiny_threshold.py 200 2>&1 | tail -3
-timeout 600 MGK_SERIAL=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv python tools/prof_c5.py 3000 > /dev/null 2>&1
+MGK_SERIAL=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv python tools/prof_c5.py 3000 > /dev/null 2>&1
 grep -E "k_pcg" gpurun_out/launches_c5.csv | awk -F'","' '{print $5, $(NF)}' | cut -c1-150
 MGK_PANEL_CTAS_PER_SM=1 timeout 300 python tools/probe_sizes.py 296 0 2>&1 | grep -E "pairs/s"
