@@ -786,7 +786,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
       ctas[k] = 2 * c->num_sms;
     } else if (j.kernel == JK_PANEL) {
       const int64_t nm = j.max_n * j.max_m;
-      slabs[k] = 5 * ((nm + 31) / 32 * 32);
+      slabs[k] = 6 * ((nm + 31) / 32 * 32);
       // P and Ap in shared memory when every pair of the job fits; else all pairs keep them in HBM/L2
       // and the whole L1 stays available to the gathers
       const int64_t smem_nm = getenv("MGK_PANEL_SMEM_NM") ? atoll(getenv("MGK_PANEL_SMEM_NM")) : kPanelSmemNM;
@@ -807,7 +807,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   for (auto& j : jobs)
     if (j.kernel == JK_GRID && j.job.npairs > 0) grid_vstride = std::max(grid_vstride, (j.max_n * j.max_m + 31) / 32 * 32);
   if (grid_vstride > 0) {
-    CUDA_TRY(c->d_gridvec.alloc((size_t)(5 * grid_vstride)));
+    CUDA_TRY(c->d_gridvec.alloc((size_t)(6 * grid_vstride)));
     CUDA_TRY(c->d_gridbuf.alloc((size_t)(2 * gblocks)));
   }
   c->last_launches = 0;
@@ -935,6 +935,22 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
     tcol[u] = (int32_t)split;
     tpre[u + 1] = tpre[u] + (ns - split);
   }
+  // mid x mid pairs split the same way by n_u * n_v <= kPanelSmemNM: the second part keeps P and Ap in
+  // shared memory, the first streams them through L1/L2
+  std::vector<int64_t> bpre(nmid + 1, 0), spre(nmid + 1, 0);
+  std::vector<int32_t> bcol(nmid), scol(nmid);
+  for (int64_t u = 0; u < nmid; ++u) {
+    const int64_t nu = c->graphs[mid[u]].n;
+    int64_t lo = u, hi = nmid;
+    while (lo < hi) {
+      const int64_t md = (lo + hi) / 2;
+      if ((int64_t)c->graphs[mid[md]].n * nu > kPanelSmemNM) lo = md + 1; else hi = md;
+    }
+    bcol[u] = (int32_t)u;
+    bpre[u + 1] = bpre[u] + (lo - u);
+    scol[u] = (int32_t)lo;
+    spre[u + 1] = spre[u] + (nmid - lo);
+  }
   cudaStream_t s = c->stream;
   std::vector<int32_t> lists;  // small, mid, large
   lists.insert(lists.end(), small.begin(), small.end());
@@ -943,8 +959,12 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   CUDA_TRY(c->d_list_a.upload(lists, s));
   std::vector<int64_t> pre(mpre);
   pre.insert(pre.end(), tpre.begin(), tpre.end());
+  pre.insert(pre.end(), bpre.begin(), bpre.end());
+  pre.insert(pre.end(), spre.begin(), spre.end());
   std::vector<int32_t> col(mcol);
   col.insert(col.end(), tcol.begin(), tcol.end());
+  col.insert(col.end(), bcol.begin(), bcol.end());
+  col.insert(col.end(), scol.begin(), scol.end());
   CUDA_TRY(c->d_rowpre.upload(pre, s));
   CUDA_TRY(c->d_rowcol.upload(col, s));
   c->h_lists = lists;
@@ -991,9 +1011,20 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   jt.job = PairJob{PM_RAGGED, (int32_t)ns, 0, tpre[ns], 0, 1, dsmall, nullptr, c->d_rowpre.ptr + ns + 1,
                    c->d_rowcol.ptr + ns};
   jt.kernel = JK_TINY;
+  JobSpec jmb = tri(mid, dmid, cta), jms = tri(mid, dmid, cta);
+  if (cta == JK_PANEL) {
+    const int64_t* bp = c->d_rowpre.ptr + 2 * (ns + 1);
+    const int32_t* bc = c->d_rowcol.ptr + 2 * ns;
+    jmb.job = PairJob{PM_RAGGED, (int32_t)nmid, 0, bpre[nmid], 0, 1, dmid, nullptr, bp, bc};
+    jms.job = PairJob{PM_RAGGED, (int32_t)nmid, 0, spre[nmid], 0, 1, dmid, nullptr, bp + nmid + 1, bc + nmid};
+    jms.max_n = std::min<int64_t>(jms.max_n * jms.max_m, kPanelSmemNM);  // every pair has n m <= kPanelSmemNM
+    jms.max_m = 1;
+  } else {
+    jms.job.npairs = 0;
+  }
   // big pairs first (longest job first across classes)
   jobs = {tri(large, dlarge, JK_GRID), rect(large, dlarge, mid, dmid, cta), rect(large, dlarge, small, dsmall, cta),
-          tri(mid, dmid, cta), rect(mid, dmid, small, dsmall, cta), jw, jm, jt};
+          jmb, jms, rect(mid, dmid, small, dsmall, cta), jw, jm, jt};
   return MGK_OK;
 }
 

@@ -284,6 +284,106 @@ __device__ __forceinline__ void xmv_dispatch(int ns, const KernelDesc& ek, const
   }
 }
 
+// Unlabeled pairs (kappa_e = 1): the off-diagonal block is A (x) B, so
+// XMV(P) = A P B^T (the factorisation of the reference's unlabeled dense x dense
+// micro-kernel, product.py:94) at n S_L + S_U m work instead of S_U S_L:
+//   phase T:  T[j][r] = sum_{t in L(r)} w'_t P[j][col(t)]  (warp items over P rows x L panels,
+//             the panel's slots in registers, segment sums as in xmv_panels)
+//   phase AP: AP[i][r] = diag P - sum_{k in U(i)} w_k T[j_k][r]  (thread per element, coalesced over r)
+// The caller places a block / grid barrier between the phases.
+template <int NS>
+__device__ void factored_T(const PairView& v, const float* P, float* T, float* SEG, int lane, int64_t w0,
+                           int64_t wstride) {
+  const int n = v.n, m = v.m;
+  const int nchunks = (n + v.rpc - 1) / v.rpc;
+  const int64_t items = (int64_t)v.np * nchunks;
+  for (int64_t item = w0; item < items; item += wstride) {
+    const int p = (int)(item / nchunks), c = (int)(item - (int64_t)p * nchunks);
+    const int rbeg = v.prow ? v.prow[p] : 0;
+    const int rend = v.prow ? v.prow[p + 1] : m;
+    const int kbeg = v.lrp[rbeg], kend = v.lrp[rend];
+    int lcol[NS];
+    float lw[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const int k = kbeg + lane + 32 * t;
+      lcol[t] = 0;
+      lw[t] = 0.0f;
+      if (k < kend) {
+        const float4 e = v.le[k];
+        lcol[t] = __float_as_int(e.x);
+        lw[t] = e.y;
+      }
+    }
+    const int j0 = c * v.rpc, j1 = min(n, j0 + v.rpc);
+    for (int j = j0; j < j1; j += 2) {
+      const bool two = j + 1 < j1;
+      const float* r0 = P + j * m;
+      const float* r1 = two ? r0 + m : r0;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        SEG[lane + 32 * t] = lw[t] * r0[lcol[t]];
+        SEG[kPanelCap + lane + 32 * t] = lw[t] * r1[lcol[t]];
+      }
+      __syncwarp();
+      for (int r = rbeg + lane; r < rend; r += 32) {
+        const int q0 = v.lrp[r] - kbeg, q1 = v.lrp[r + 1] - kbeg;
+        float s0 = 0.0f, s1 = 0.0f;
+        for (int q = q0; q < q1; ++q) {
+          s0 += SEG[q];
+          s1 += SEG[kPanelCap + q];
+        }
+        T[j * m + r] = s0;
+        if (two) T[(j + 1) * m + r] = s1;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ void factored_T_dispatch(int ns, const PairView& v, const float* P, float* T, float* SEG,
+                                                    int lane, int64_t w0, int64_t wstride) {
+  switch (ns) {
+    case 2: factored_T<2>(v, P, T, SEG, lane, w0, wstride); break;
+    case 4: factored_T<4>(v, P, T, SEG, lane, w0, wstride); break;
+    default: factored_T<kPanelSlots>(v, P, T, SEG, lane, w0, wstride); break;
+  }
+}
+
+// AP = diag P - A T over elements e0, e0 + estride, ...; accumulates (p.Ap, px.p) when part != nullptr.
+__device__ void factored_AP(const PairView& v, const float* P, const float* T, float* AP, const float* DG,
+                            int64_t e0, int64_t estride, const float* pu, const float* pl, double2* part) {
+  const int m = v.m;
+  const int64_t nm = (int64_t)v.n * m;
+  const int64_t di = estride / m, dl = estride % m;
+  int64_t i = e0 / m, l = e0 % m;
+  double pap = 0.0, pxp = 0.0;
+  for (int64_t e = e0; e < nm; e += estride) {
+    float acc = 0.0f;
+    for (int k = v.urp[i]; k < v.urp[i + 1]; ++k) {
+      const float4 u = v.ue[k];
+      acc = fmaf(u.y, T[(int64_t)__float_as_int(u.x) * m + l], acc);
+    }
+    const float p = P[e];
+    const float ap = fmaf(DG[e], p, -acc);
+    AP[e] = ap;
+    if (part) {
+      pap += (double)p * (double)ap;
+      pxp += (double)(pu[i] * pl[l]) * (double)p;
+    }
+    l += dl;
+    i += di;
+    if (l >= m) {
+      l -= m;
+      ++i;
+    }
+  }
+  if (part) {
+    part->x += pap;
+    part->y += pxp;
+  }
+}
+
 // Lane-side cost of a graph (slot-rounded nonzeros a warp streams per U nonzero).
 __device__ __forceinline__ int64_t lane_cost(const GraphDesc& g) {
   const int S = 2 * g.ne;
@@ -304,7 +404,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
   float* SEG = psm + warp * kSegFloats;
   float* svec = psm + kPW * kSegFloats;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
-  const int64_t vstride = slab / 5;
+  const int64_t vstride = slab / 6;
 
   for (;;) {
     if (threadIdx.x == 0) sh_pid = atomicAdd(queue, 1ull);
@@ -346,6 +446,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     float* X = base + 2 * vstride;
     float* P = base + 3 * vstride;
     float* AP = base + 4 * vstride;
+    float* T = base + 5 * vstride;  // unlabeled: P B^T
     if (2 * nm <= smem_vec) {
       P = svec;
       AP = svec + nm;
@@ -400,12 +501,21 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     int64_t it = 0;
     double value = 0.0;
     const bool self_pair = (ga == gb);
+    // unlabeled: factorise when it saves work beyond its extra pass (not for degree-4 sparsity)
+    const bool factor = (int64_t)(2 * U.ne) * SL > 3 * ((int64_t)n * SL + (int64_t)(2 * U.ne) * m);
     __syncthreads();
 
     while (!conv && it < max_iter) {
       double2 part = make_double2(0.0, 0.0);
-      xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, warp, kPW, ds.p + U.node_off, ds.p + L.node_off,
-                       self_pair ? nullptr : &part);
+      if (EK == KK_NONE && factor) {
+        factored_T_dispatch(ns, v, P, T, SEG, lane, warp, kPW);
+        __syncthreads();
+        factored_AP(v, P, T, AP, DG, threadIdx.x, kPT, ds.p + U.node_off, ds.p + L.node_off,
+                    self_pair ? nullptr : &part);
+      } else {
+        xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, warp, kPW, ds.p + U.node_off, ds.p + L.node_off,
+                         self_pair ? nullptr : &part);
+      }
       __syncthreads();
       if (self_pair) {
         // self pair: keep the iterate exactly symmetric (see pcg_warp.cu)
@@ -622,6 +732,7 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
   float* X = vec + 2 * vstride;
   float* P = vec + 3 * vstride;
   float* AP = vec + 4 * vstride;
+  float* T = vec + 5 * vstride;  // unlabeled: P B^T
   int flip = 0;
   auto gsum = [&](double2 v) {
     double2 r = grid_sum2(v, gbuf + flip * gridDim.x, wred, &sres, grid);
@@ -697,11 +808,19 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int64_t it = 0;
     double value = 0.0;
     const bool self_pair = (ga == gb);
+    const bool factor = (int64_t)(2 * U.ne) * SL > 3 * ((int64_t)n * SL + (int64_t)(2 * U.ne) * m);
 
     while (!conv && it < max_iter) {
       double2 part = make_double2(0.0, 0.0);
-      xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, gw, GW, ds.p + U.node_off, ds.p + L.node_off,
-                       self_pair ? nullptr : &part);
+      if (EK == KK_NONE && factor) {
+        factored_T_dispatch(ns, v, P, T, SEG, lane, gw, GW);
+        grid.sync();
+        factored_AP(v, P, T, AP, DG, gtid, gthreads, ds.p + U.node_off, ds.p + L.node_off,
+                    self_pair ? nullptr : &part);
+      } else {
+        xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, gw, GW, ds.p + U.node_off, ds.p + L.node_off,
+                         self_pair ? nullptr : &part);
+      }
       if (self_pair) {
         grid.sync();
         for (int64_t e = gtid; e < nm; e += gthreads) {
