@@ -38,7 +38,12 @@ namespace cg = cooperative_groups;
 constexpr int kPT = MGK_PANEL_THREADS;  // threads per CTA
 constexpr int kPW = kPT / 32;     // warps per CTA
 constexpr int kSegFloats = 2 * kPanelCap;  // per-warp segment buffer (two U rows)
-constexpr int kPanelStaticSmem = kPW * kSegFloats * 4;
+// Per-CTA cache of small graphs' row expansions (U up to kCacheU nonzeros, a single-panel L), so the
+// XMV's row entries come from shared memory instead of L1/L2 on mid-size pairs.
+constexpr int kCacheU = 1024;
+constexpr int kCacheRows = 256;
+constexpr int kCacheFloats = 4 * (kCacheU + kPanelCap) + 2 * (kCacheRows + 1) + 2;
+constexpr int kPanelStaticSmem = (kPW * kSegFloats + kCacheFloats) * 4;
 
 __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -402,7 +407,11 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
   __shared__ unsigned long long sh_pid;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* SEG = psm + warp * kSegFloats;
-  float* svec = psm + kPW * kSegFloats;
+  float4* c_ue = reinterpret_cast<float4*>(psm + kPW * kSegFloats);
+  float4* c_le = c_ue + kCacheU;
+  int32_t* c_urp = reinterpret_cast<int32_t*>(c_le + kPanelCap);
+  int32_t* c_lrp = c_urp + kCacheRows + 1;
+  float* svec = psm + kPW * kSegFloats + kCacheFloats;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
   const int64_t vstride = slab / 6;
 
@@ -438,6 +447,30 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
       rpc = rpc < 2 ? 2 : (rpc > 32 ? 32 : rpc);
       if (prm.panel_rpc > 0) rpc = prm.panel_rpc;
       v.rpc = (rpc + 1) & ~1;
+    }
+    // stage the row expansions in shared memory when they fit (the previous pair is done with them:
+    // the pair loop ends on a barrier)
+    {
+      const int SU = 2 * U.ne;
+      const bool cu = SU <= kCacheU && n < kCacheRows;
+      const bool cl = v.np == 1 && SL <= kPanelCap && m < kCacheRows;
+      if (cu) {
+        for (int k = threadIdx.x; k < SU; k += kPT) c_ue[k] = v.ue[k];
+        for (int r = threadIdx.x; r <= n; r += kPT) c_urp[r] = v.urp[r];
+      }
+      if (cl) {
+        for (int k = threadIdx.x; k < SL; k += kPT) c_le[k] = v.le[k];
+        for (int r = threadIdx.x; r <= m; r += kPT) c_lrp[r] = v.lrp[r];
+      }
+      __syncthreads();
+      if (cu) {
+        v.ue = c_ue;
+        v.urp = c_urp;
+      }
+      if (cl) {
+        v.le = c_le;
+        v.lrp = c_lrp;
+      }
     }
 
     float* base = scratch + (int64_t)blockIdx.x * slab;
