@@ -243,7 +243,7 @@ class ClockSampler:
 
 def traffic_from_profiles(cfg: Config):
     """dram bytes per launch of the solver kernel from the committed ncu capture of this config, if any."""
-    for p in sorted((ROOT / "profiles").glob(f"*ncu_summary_c{cfg.key}*.json"), reverse=True):
+    for p in sorted((ROOT / "profiles").glob(f"*ncu_summary_c{cfg.key}.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
             return d.get("solver_dram_bytes_per_launch"), p.name
