@@ -213,16 +213,27 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
       if (e < nm) {
-        double acc = 0.0;
+        // two independent FP64 chains (even / odd L nonzeros) shorten the dependent DFMA latency
+        double acc = 0.0, acc2 = 0.0;
         for (int k = k0[s]; k < k1[s]; ++k) {
           const float2 a = uwl[k];
           const double* prow = P + (uoff[k] >> 7) * m;
-          for (int q = q0[s]; q < q1[s]; ++q) {
+          int q = q0[s];
+          for (; q + 1 < q1[s]; q += 2) {
+            const float4 b0 = le[q], b1 = le[q + 1];
+            const double p0 = prow[__float_as_int(b0.x)], p1 = prow[__float_as_int(b1.x)];
+            const float c0 = edge_kappa<EK>(ek, a.y, b0.z) * a.x * b0.y;
+            const float c1 = edge_kappa<EK>(ek, a.y, b1.z) * a.x * b1.y;
+            acc = fma((double)c0, p0, acc);
+            acc2 = fma((double)c1, p1, acc2);
+          }
+          if (q < q1[s]) {
             const float4 b = le[q];
             const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
             acc = fma((double)c, prow[__float_as_int(b.x)], acc);
           }
         }
+        acc += acc2;
         const double p = P[e];
         ap[s] = dg[s] * p - acc;
         pap += p * ap[s];
@@ -615,7 +626,7 @@ struct TinySmem {
 };
 
 template <int EK>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
 k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
            unsigned long long* queue) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
