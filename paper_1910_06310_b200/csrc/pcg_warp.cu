@@ -154,14 +154,12 @@ constexpr int kTinyMax = 128;
 template <int EK>
 __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
                            const GraphDesc& U, const GraphDesc& L, const float2* uwl, const int* uoff,
-                           const int* urow, const float4* le, const int* lrow, double* P, int lane,
-                           double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw, bool swap) {
+                           const int* urow, const float4* le, const int* lrow, double* P, double* AP, double* DG,
+                           int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw,
+                           bool swap) {
   const int nu = U.n, m = L.n, nm = nu * m;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
-  // the lane's elements e = lane + 32 s (s < 4) are private: residual, iterate, A p, the
-  // diagonal and its inverse stay in registers; only the direction P is shared (gathered)
-  double r[4], x[4], ap[4], dg[4], idg[4];
-  int ei[4], k0[4], k1[4], q0[4], q1[4];
+  double r[4], x[4];
   double bb_u = 0.0, bb_l = 0.0;
   if (lane < nu) {
     double dq = ds.deg[U.node_off + lane] * (double)ds.q[U.node_off + lane];
@@ -177,24 +175,14 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
     const int e = lane + 32 * s;
     r[s] = 0.0;
     x[s] = 0.0;
-    ap[s] = 0.0;
-    dg[s] = 1.0;
-    idg[s] = 1.0;
-    ei[s] = 0;
-    k0[s] = k1[s] = q0[s] = q1[s] = 0;
     if (e < nm) {
       const int i = e / m, l = e - i * m;
-      ei[s] = i;
-      k0[s] = urow[i];
-      k1[s] = urow[i + 1];
-      q0[s] = lrow[l];
-      q1[s] = lrow[l + 1];
       const int64_t vu = U.node_off + i, vl = L.node_off + l;
-      dg[s] = diag_of(ds, vk, prm, vlab, vu, vl);
-      idg[s] = 1.0 / dg[s];
+      const double dg = diag_of(ds, vk, prm, vlab, vu, vl);
       const double b = (ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]);
+      DG[e] = dg;
       r[s] = b;
-      const double z = b * idg[s];
+      const double z = b / dg;
       P[e] = z;
       rho += b * z;
       rr += b * b;
@@ -208,38 +196,32 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
   int64_t it = 0;
   __syncwarp();
   while (!conv && it < max_iter) {
-    double pap = 0.0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
       if (e < nm) {
-        // two independent FP64 chains (even / odd L nonzeros) shorten the dependent DFMA latency
-        double acc = 0.0, acc2 = 0.0;
-        for (int k = k0[s]; k < k1[s]; ++k) {
+        const int i = e / m, l = e - i * m;
+        double acc = 0.0;
+        for (int k = urow[i]; k < urow[i + 1]; ++k) {
           const float2 a = uwl[k];
           const double* prow = P + (uoff[k] >> 7) * m;
-          int q = q0[s];
-          for (; q + 1 < q1[s]; q += 2) {
-            const float4 b0 = le[q], b1 = le[q + 1];
-            const double p0 = prow[__float_as_int(b0.x)], p1 = prow[__float_as_int(b1.x)];
-            const float c0 = edge_kappa<EK>(ek, a.y, b0.z) * a.x * b0.y;
-            const float c1 = edge_kappa<EK>(ek, a.y, b1.z) * a.x * b1.y;
-            acc = fma((double)c0, p0, acc);
-            acc2 = fma((double)c1, p1, acc2);
-          }
-          if (q < q1[s]) {
+          for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
             const float4 b = le[q];
             const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
             acc = fma((double)c, prow[__float_as_int(b.x)], acc);
           }
         }
-        acc += acc2;
-        const double p = P[e];
-        ap[s] = dg[s] * p - acc;
-        pap += p * ap[s];
+        AP[e] = DG[e] * P[e] - acc;
       }
     }
+    __syncwarp();
     ++it;
+    double pap = 0.0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int e = lane + 32 * s;
+      if (e < nm) pap += P[e] * AP[e];
+    }
     const double alpha = rho / warp_sum(pap);
     double rr_l = 0.0, rz_l = 0.0;
 #pragma unroll
@@ -247,9 +229,9 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       const int e = lane + 32 * s;
       if (e < nm) {
         x[s] += alpha * P[e];
-        r[s] -= alpha * ap[s];
+        r[s] -= alpha * AP[e];
         rr_l += r[s] * r[s];
-        rz_l += r[s] * (r[s] * idg[s]);
+        rz_l += r[s] * (r[s] / DG[e]);
       }
     }
     rr = warp_sum(rr_l);
@@ -259,11 +241,11 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       break;
     }
     const double beta = rho_next / rho;
-    __syncwarp();  // every lane has finished gathering P
+    __syncwarp();
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
-      if (e < nm) P[e] = r[s] * idg[s] + beta * P[e];
+      if (e < nm) P[e] = r[s] / DG[e] + beta * P[e];
     }
     rho = rho_next;
     __syncwarp();
@@ -620,13 +602,13 @@ struct TinySmem {
   float2 UWL[SMAX];
   int UOFF[SMAX];
   float4 LE[SMAX];
-  double P[kTinyMax];      // PCG direction (the only shared vector)
+  double V[3 * kTinyMax];  // P, AP, DG
   int urow[NU + 8];
   int lrow[40];
 };
 
 template <int EK>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
            unsigned long long* queue) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -653,8 +635,8 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int64_t it;
     bool conv;
     float* nw = out.nodewise ? out.nodewise + out.nodewise_off[pid] : nullptr;
-    solve_tiny<EK>(ds, vk, ek, prm, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.P, lane, val, it, conv, rr, nw,
-                   false);
+    solve_tiny<EK>(ds, vk, ek, prm, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.V, S.V + kTinyMax,
+                   S.V + 2 * kTinyMax, lane, val, it, conv, rr, nw, false);
     write_pair_outputs(out, pid, ga, gb, val, it, conv, rr, lane);
     __syncwarp();
   }
