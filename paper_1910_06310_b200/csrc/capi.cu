@@ -310,8 +310,8 @@ struct mgk_ctx {
   // host images of the Gram job lists (host-side pair decoding for streaming)
   std::vector<int32_t> h_lists, h_rowcol;
   std::vector<int64_t> h_rowpre;
-  // pinned staging for streamed nodewise chunks
-  float* h_nw = nullptr;
+  // pinned staging for streamed nodewise chunks (two slots: fields + per-pair records)
+  void* h_nw = nullptr;
   size_t h_nw_cap = 0;
 };
 
@@ -766,9 +766,14 @@ static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, in
   return (f + 31) / 32 * 32;
 }
 
+// Enqueue every job of `jobs` (device time bracketed by e0 / e1, default the context's events); with
+// sync the call waits for completion and stores the elapsed time in last_ms.
 static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_base,
-                    const std::vector<int64_t>& out_offsets, const SolveParams& prm) {
+                    const std::vector<int64_t>& out_offsets, const SolveParams& prm, bool sync = true,
+                    cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr) {
   cudaStream_t s = c->stream;
+  if (!e0) e0 = c->ev0;
+  if (!e1) e1 = c->ev1;
   CUDA_TRY(c->d_queue.alloc(std::max<size_t>(jobs.size(), 1)));
   CUDA_TRY(cudaMemsetAsync(c->d_queue.ptr, 0, std::max<size_t>(jobs.size(), 1) * sizeof(unsigned long long), s));
   // scratch slabs (block and panel jobs run one after another on the stream and share the buffer)
@@ -811,7 +816,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     CUDA_TRY(c->d_gridbuf.alloc((size_t)(2 * gblocks)));
   }
   c->last_launches = 0;
-  CUDA_TRY(cudaEventRecord(c->ev0, s));
+  CUDA_TRY(cudaEventRecord(e0, s));
   // Streams: grid and CTA-class jobs in order on the main stream (they share the scratch slabs and the
   // cooperative grid must own the device); warp-class jobs on side stream 0, tiny jobs on side stream
   // 1.  Persistent kernels leave the device as their queues drain, so the concurrent jobs fill each
@@ -871,11 +876,12 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     CUDA_TRY(cudaStreamWaitEvent(s, c->evside[q], 0));
   }
   (void)used;
-  CUDA_TRY(cudaEventRecord(c->ev1, s));
-  CUDA_TRY(cudaEventSynchronize(c->ev1));
+  CUDA_TRY(cudaEventRecord(e1, s));
+  if (!sync) return MGK_OK;
+  CUDA_TRY(cudaEventSynchronize(e1));
   CUDA_TRY(cudaGetLastError());
   float ms = 0.0f;
-  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  cudaEventElapsedTime(&ms, e0, e1);
   c->last_ms = ms;
   return MGK_OK;
 }
@@ -1147,79 +1153,159 @@ int mgk_gram_nodewise(mgk_ctx* c, int rank, int world, double tol, int64_t max_i
   max_pair *= max_pair;
   const int64_t cap = std::max<int64_t>(chunk_bytes / 4, max_pair);
   const int64_t pair_cap = 1 << 22;
-  if (c->h_nw_cap < (size_t)cap) {
+  // Two slots: the device solves chunk k + 1 while the host hands chunk k (already copied into pinned
+  // memory) to the sink.  Per slot: field floats, per-pair records, offsets.
+  constexpr int64_t kRec = 4 + 4 + 8 + 4 + 1;  // a, b, value, iterations, converged
+  const size_t host_need = (size_t)(2 * cap) * sizeof(float) + (size_t)(2 * pair_cap) * kRec;
+  if (c->h_nw_cap < host_need) {
     if (c->h_nw) cudaFreeHost(c->h_nw);
     c->h_nw = nullptr;
     c->h_nw_cap = 0;
-    CUDA_TRY(cudaMallocHost(&c->h_nw, (size_t)cap * sizeof(float)));
-    c->h_nw_cap = (size_t)cap;
+    CUDA_TRY(cudaMallocHost(&c->h_nw, host_need));
+    c->h_nw_cap = host_need;
   }
-  CUDA_TRY(c->d_nodewise.alloc(cap));
-  CUDA_TRY(c->d_value.alloc(pair_cap));
-  CUDA_TRY(c->d_iters.alloc(pair_cap));
-  CUDA_TRY(c->d_conv.alloc(pair_cap));
-  CUDA_TRY(c->d_pa.alloc(pair_cap));
-  CUDA_TRY(c->d_pb.alloc(pair_cap));
-  std::vector<int64_t> offs;
-  std::vector<int32_t> ha, hb, hi;
-  std::vector<double> hv;
-  std::vector<uint8_t> hc;
+  CUDA_TRY(c->d_nodewise.alloc(2 * cap));
+  CUDA_TRY(c->d_value.alloc(2 * pair_cap));
+  CUDA_TRY(c->d_iters.alloc(2 * pair_cap));
+  CUDA_TRY(c->d_conv.alloc(2 * pair_cap));
+  CUDA_TRY(c->d_pa.alloc(2 * pair_cap));
+  CUDA_TRY(c->d_pb.alloc(2 * pair_cap));
+  CUDA_TRY(c->d_nwoff.alloc(2 * (pair_cap + 1)));
+  struct Slot {
+    float* nw;
+    int32_t *a, *b, *it;
+    double* v;
+    uint8_t* cv;
+    std::vector<int64_t> offs;
+    int64_t np = 0;
+    cudaEvent_t t0 = nullptr, t1 = nullptr, done = nullptr;
+  } slot[2];
+  {
+    char* h = reinterpret_cast<char*>(c->h_nw);
+    for (int k = 0; k < 2; ++k) {
+      slot[k].nw = reinterpret_cast<float*>(h) + k * cap;
+    }
+    char* r = h + (size_t)(2 * cap) * sizeof(float);
+    for (int k = 0; k < 2; ++k) {
+      slot[k].v = reinterpret_cast<double*>(r);
+      r += pair_cap * 8;
+      slot[k].a = reinterpret_cast<int32_t*>(r);
+      r += pair_cap * 4;
+      slot[k].b = reinterpret_cast<int32_t*>(r);
+      r += pair_cap * 4;
+      slot[k].it = reinterpret_cast<int32_t*>(r);
+      r += pair_cap * 4;
+      slot[k].cv = reinterpret_cast<uint8_t*>(r);
+      r += pair_cap;
+    }
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaEventCreate(&slot[k].t0));
+      CUDA_TRY(cudaEventCreate(&slot[k].t1));
+      CUDA_TRY(cudaEventCreateWithFlags(&slot[k].done, cudaEventDisableTiming));
+    }
+  }
+  auto destroy = [&]() {
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(slot[k].t0);
+      cudaEventDestroy(slot[k].t1);
+      cudaEventDestroy(slot[k].done);
+    }
+  };
   int64_t total_pairs = 0, total_floats = 0;
   double ms_total = 0.0;
-  int launches = 0;
+  int launches = 0, pending = -1, chunk = 0;
+  cudaStream_t s = c->stream;
+  // hand a finished slot to the sink
+  auto drain = [&](int k) -> int {
+    Slot& z = slot[k];
+    cudaError_t e = cudaEventSynchronize(z.done);
+    if (e != cudaSuccess) return fail(MGK_E_CUDA, "nodewise stream: %s", cudaGetErrorString(e));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, z.t0, z.t1);
+    ms_total += ms;
+    if (sink(user, z.np, z.a, z.b, z.v, z.it, z.cv, z.offs.data(), z.nw) != 0)
+      return fail(MGK_E_STATE, "nodewise sink aborted the stream");
+    total_pairs += z.np;
+    total_floats += z.offs.back();
+    return MGK_OK;
+  };
   for (const JobSpec& js : jobs) {
     if (js.job.npairs <= 0) continue;
     const PairJob hj = host_job(c, js.job);
     const int64_t local = shard_len(js.job.npairs, rank, world);
-    for (int64_t q0 = 0; q0 < local;) {
+    for (int64_t q0 = 0; q0 < local; ++chunk) {
+      const int k = chunk & 1;
+      Slot& z = slot[k];
       // chunk [q0, q1): field floats <= cap and pairs <= pair_cap
-      offs.assign(1, 0);
+      z.offs.assign(1, 0);
       int64_t q1 = q0;
       while (q1 < local && q1 - q0 < pair_cap) {
         int32_t a, b;
         decode_pair(hj, rank + q1 * (int64_t)world, a, b);
         const int64_t f = (int64_t)c->graphs[a].n * c->graphs[b].n;
-        if (offs.back() + f > cap) break;
-        offs.push_back(offs.back() + f);
+        if (z.offs.back() + f > cap) break;
+        z.offs.push_back(z.offs.back() + f);
         ++q1;
       }
-      const int64_t np = q1 - q0;
-      CUDA_TRY(c->d_nwoff.upload(offs, c->stream));
-      JobSpec chunk = js;
-      chunk.job.offset = rank + q0 * (int64_t)world;
-      chunk.job.stride = world;
-      chunk.job.npairs = np;
-      std::vector<JobSpec> one = {chunk};
+      z.np = q1 - q0;
+      int64_t* d_off = c->d_nwoff.ptr + k * (pair_cap + 1);
+      CUDA_TRY(cudaMemcpyAsync(d_off, z.offs.data(), z.offs.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      g_h2d_bytes += (int64_t)(z.offs.size() * sizeof(int64_t));
+      JobSpec chunkjob = js;
+      chunkjob.job.offset = rank + q0 * (int64_t)world;
+      chunkjob.job.stride = world;
+      chunkjob.job.npairs = z.np;
+      std::vector<JobSpec> one = {chunkjob};
       SolveOut o{};
-      o.value = c->d_value.ptr;
-      o.iters = c->d_iters.ptr;
-      o.conv = c->d_conv.ptr;
-      o.pair_a = c->d_pa.ptr;
-      o.pair_b = c->d_pb.ptr;
-      o.nodewise = c->d_nodewise.ptr;
-      o.nodewise_off = c->d_nwoff.ptr;
-      rc = run_jobs(c, one, o, {0}, prm);
-      if (rc) return rc;
-      ms_total += c->last_ms;
+      o.value = c->d_value.ptr + k * pair_cap;
+      o.iters = c->d_iters.ptr + k * pair_cap;
+      o.conv = c->d_conv.ptr + k * pair_cap;
+      o.pair_a = c->d_pa.ptr + k * pair_cap;
+      o.pair_b = c->d_pb.ptr + k * pair_cap;
+      o.nodewise = c->d_nodewise.ptr + k * cap;
+      o.nodewise_off = d_off;
+      rc = run_jobs(c, one, o, {0}, prm, false, z.t0, z.t1);
+      if (rc) {
+        destroy();
+        return rc;
+      }
       launches += c->last_launches;
-      ha.resize(np);
-      hb.resize(np);
-      hi.resize(np);
-      hv.resize(np);
-      hc.resize(np);
-      CUDA_TRY(d2h(ha.data(), c->d_pa.ptr, np * sizeof(int32_t)));
-      CUDA_TRY(d2h(hb.data(), c->d_pb.ptr, np * sizeof(int32_t)));
-      CUDA_TRY(d2h(hv.data(), c->d_value.ptr, np * sizeof(double)));
-      CUDA_TRY(d2h(hi.data(), c->d_iters.ptr, np * sizeof(int32_t)));
-      CUDA_TRY(d2h(hc.data(), c->d_conv.ptr, np));
-      CUDA_TRY(d2h(c->h_nw, c->d_nodewise.ptr, offs.back() * sizeof(float)));
-      if (sink(user, np, ha.data(), hb.data(), hv.data(), hi.data(), hc.data(), offs.data(), c->h_nw) != 0)
-        return fail(MGK_E_STATE, "nodewise sink aborted the stream");
-      total_pairs += np;
-      total_floats += offs.back();
+      const int64_t np = z.np;
+      auto cp = [&](void* dst, const void* src, size_t bytes) {
+        g_d2h_bytes += (int64_t)bytes;
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+      };
+      cudaError_t e = cp(z.a, o.pair_a, np * 4);
+      if (e == cudaSuccess) e = cp(z.b, o.pair_b, np * 4);
+      if (e == cudaSuccess) e = cp(z.v, o.value, np * 8);
+      if (e == cudaSuccess) e = cp(z.it, o.iters, np * 4);
+      if (e == cudaSuccess) e = cp(z.cv, o.conv, np);
+      if (e == cudaSuccess) e = cp(z.nw, o.nodewise, z.offs.back() * sizeof(float));
+      if (e == cudaSuccess) e = cudaEventRecord(z.done, s);
+      if (e != cudaSuccess) {
+        destroy();
+        return fail(MGK_E_CUDA, "nodewise stream: %s", cudaGetErrorString(e));
+      }
+      if (pending >= 0) {
+        rc = drain(pending);
+        if (rc) {
+          cudaStreamSynchronize(s);
+          destroy();
+          return rc;
+        }
+      }
+      pending = k;
       q0 = q1;
     }
   }
+  if (pending >= 0) {
+    rc = drain(pending);
+    if (rc) {
+      destroy();
+      return rc;
+    }
+  }
+  destroy();
   c->last_ms = ms_total;
   c->last_launches = launches;
   if (npairs_out) *npairs_out = total_pairs;
