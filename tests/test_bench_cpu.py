@@ -39,3 +39,10 @@ def test_factored_system_matches_coo_plan():
         a = O.solve_pcg(ga, gb, tol=1e-8)
         b = O.solve_pcg(ga, gb, tol=1e-8, system=fac)
         assert a.iterations == b.iterations and abs(a.value - b.value) <= 1e-12 * abs(a.value)
+
+
+def test_octile_count_matches_oracle():
+    from paper_1910_06310_b200 import synth
+
+    for g in synth.config2(count=40) + synth.config3(count=2, n_lo=200, n_hi=220):
+        assert bench.octile_count(g) == O.build_octiles(g).count
