@@ -282,6 +282,26 @@ def test_stream_nodewise_vs_oracle(mgk):
         assert np.max(np.abs(field - o.nodewise)) <= REL * np.max(np.abs(o.nodewise)), (a, b)
 
 
+def test_stream_nodewise_consumer_error(mgk):
+    """A consumer exception stops the stream, surfaces in Python, and leaves the context usable."""
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(22)
+    ds = [synth.molecule(rng, int(n)) for n in (6, 9, 12, 15, 20)]
+    calls = []
+
+    def boom(a, b, v, it, cv, off, f):
+        calls.append(len(a))
+        if len(calls) == 2:
+            raise RuntimeError("consumer stop")
+
+    with pytest.raises(RuntimeError, match="consumer stop"):
+        mgk.stream_nodewise(ds, boom, "delta:0.5", "se:1.0", chunk_bytes=4 * 200)
+    assert len(calls) == 2
+    res = mgk.compute_gram(ds, "delta:0.5", "se:1.0")
+    assert np.all(res.converged)
+
+
 def test_panel_unlabeled_rgg_vs_oracle(mgk):
     """Config-4 shape (random geometric graphs, unlabeled, tol 1e-6 per SURVEY H1) at reduced n."""
     from paper_1910_06310_b200 import synth
