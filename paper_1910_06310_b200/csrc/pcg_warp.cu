@@ -441,12 +441,20 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     const int ns = (SL + 31) >> 5;
 
     // ---- prologue: octiles -> rows (U into UE, L staged then held in registers)
-    octiles_to_rows(ds, U, lane, S.urow, el_dim, [&](int pos, int col, float w, float lab) {
-      S.UE[pos] = make_float4(weight_form<EK>(w), lab, __int_as_float(col * 128), 0.0f);
-    });
-    octiles_to_rows(ds, L, lane, S.lrow, el_dim, [&](int pos, int col, float w, float lab) {
-      stage[pos] = make_float4(__int_as_float(col), w, lab, 0.0f);
-    });
+    // rows from the dataset's row expansion of the octiles (k_rows_fill: {col, w, label, log2 w},
+    // ascending column per row): independent coalesced 16-byte loads, no per-pair bit scans
+    {
+      const float4* ur = ds.rowent + U.nz_off;
+      const float4* lr = ds.rowent + L.nz_off;
+      const int SU = 2 * U.ne;
+      for (int k = lane; k < SU; k += 32) {
+        const float4 e = ur[k];
+        S.UE[k] = make_float4(EK == KK_SE ? e.w : e.y, e.z, __int_as_float(__float_as_int(e.x) * 128), 0.0f);
+      }
+      for (int k = lane; k < SL; k += 32) stage[k] = lr[k];
+      if (lane <= nu) S.urow[lane] = ds.rowptr[U.rowptr_off + lane];
+      if (lane <= m) S.lrow[lane] = ds.rowptr[L.rowptr_off + lane];
+    }
     __syncwarp();
     int lcoff[SLM];
     float lw[SLM], llab[SLM];
