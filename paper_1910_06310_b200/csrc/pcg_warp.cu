@@ -28,9 +28,9 @@
 // S_U*S_L.  The value px.x is accumulated as sum_k alpha_k (px.p_k), so the
 // Gram path keeps no x vector.
 //
-// The octile format is what the warp reads from HBM: the prologue expands the
-// two graphs' octiles (16-byte records, one 64-bit bitmap each) into per-row
-// nonzero lists with popc/bit-scan (ascending column, as the tile order implies).
+// The graphs come from the dataset's row expansion of the device octiles
+// (k_rows_fill, tiles.cu: one popc/bit-scan pass over every tile row per
+// dataset), read per pair as coalesced 16-byte records.
 #include <cstdio>
 
 #include "mgk_internal.h"
@@ -71,40 +71,6 @@ __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
     if (lane >= o) v += u;
   }
   return v;
-}
-
-// Expand a graph's octiles into row-ordered nonzeros (lane i handles row i;
-// n <= 32); emit(pos, col, w, label) receives them, rowptr[0..n] the offsets.
-template <typename Emit>
-__device__ __forceinline__ void octiles_to_rows(const DatasetDev& ds, const GraphDesc& g, int lane, int* rowptr,
-                                                int el_dim, Emit emit) {
-  int cnt = 0;
-  const int32_t* tr = ds.trow + g.trow_off;
-  const Octile* tiles = ds.tiles + g.tile_off;
-  const int I = lane >> 3, r = lane & 7;
-  int t0 = 0, t1 = 0;
-  if (lane < g.n) {
-    t0 = tr[I];
-    t1 = tr[I + 1];
-    for (int t = t0; t < t1; ++t) cnt += __popc((uint32_t)(tiles[t].bitmap >> (8 * r)) & 0xffu);
-  }
-  const int incl = warp_incl_scan(cnt, lane);
-  int pos = incl - cnt;
-  if (lane < g.n) rowptr[lane] = pos;
-  if (lane == g.n - 1) rowptr[g.n] = incl;
-  if (lane < g.n) {
-    const float* w = ds.nz_w + g.nz_off;
-    const float* lab = ds.nz_label + g.nz_off * el_dim;
-    for (int t = t0; t < t1; ++t) {
-      const Octile o = tiles[t];
-      uint32_t byte = (uint32_t)(o.bitmap >> (8 * r)) & 0xffu;
-      const int base = o.nz_off + __popcll(o.bitmap & ((1ull << (8 * r)) - 1ull));
-      for (int c = 0; byte; ++c, byte &= byte - 1) {
-        const int k = base + c;
-        emit(pos++, o.col * 8 + (__ffs(byte) - 1), w[k], el_dim > 0 ? lab[(int64_t)k * el_dim] : 0.0f);
-      }
-    }
-  }
 }
 
 __device__ __forceinline__ void write_pair_outputs(const SolveOut& out, unsigned long long pid, int ga, int gb,
@@ -631,13 +597,19 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int32_t ga, gb;
     decode_pair(job, (int64_t)pid, ga, gb);
     const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
-    octiles_to_rows(ds, A, lane, S.urow, el_dim, [&](int pos, int col, float w, float lab) {
-      S.UWL[pos] = make_float2(w, lab);
-      S.UOFF[pos] = col * 128;
-    });
-    octiles_to_rows(ds, B, lane, S.lrow, el_dim, [&](int pos, int col, float w, float lab) {
-      S.LE[pos] = make_float4(__int_as_float(col), w, lab, 0.0f);
-    });
+    {  // rows from the dataset's row expansion of the octiles (see k_pcg_warp)
+      const float4* ar = ds.rowent + A.nz_off;
+      const float4* br = ds.rowent + B.nz_off;
+      for (int k = lane; k < 2 * A.ne; k += 32) {
+        const float4 e = ar[k];
+        S.UWL[k] = make_float2(e.y, e.z);
+        S.UOFF[k] = __float_as_int(e.x) * 128;
+      }
+      for (int k = lane; k < 2 * B.ne; k += 32) S.LE[k] = br[k];
+      if (lane <= A.n) S.urow[lane] = ds.rowptr[A.rowptr_off + lane];
+      if (lane <= B.n) S.lrow[lane] = ds.rowptr[B.rowptr_off + lane];
+    }
+    (void)el_dim;
     __syncwarp();
     double val, rr;
     int64_t it;
