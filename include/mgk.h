@@ -130,6 +130,16 @@ int mgk_gram_nodewise(mgk_ctx* ctx, int rank, int world, double tol, int64_t max
 int mgk_kernel(mgk_ctx* ctx, int32_t a, int32_t b, double tol, int64_t max_iter, double* value, double* nodewise,
                int32_t* iters, double* residual, uint8_t* conv);
 
+/* Device graph ingestion: spatial_graph (graphio.py:211-240)
+ * for N point clouds at once on CUDA device `device`.  node_off[N+1] offsets
+ * into points[sum n * dim] (dim 2 or 3, float64, row-major).  Every pair i < j
+ * with distance d < cutoff becomes an edge (i, j lexicographic, local ids),
+ * w = (1 - (d/cutoff)^2)^2, label d -- bit-identical to the reference's float64
+ * numpy evaluation.  Writes edge_off[N+1]; call with the four edge arrays NULL
+ * to size them, then again with buffers of edge_off[N] entries. */
+int mgk_spatial_edges(int device, int32_t N, const int64_t* node_off, int dim, const double* points, double cutoff,
+                      int64_t* edge_off, int32_t* ei, int32_t* ej, double* w, double* d);
+
 /* Device time (ms, CUDA events on the solver stream) and the number of
  * kernel launches of the last solve call. */
 int mgk_last_timing(mgk_ctx* ctx, double* solve_ms, int32_t* launches);

@@ -10,6 +10,7 @@ host-side mirror of the reference interface.
 from .basekernels import (BaseKernel, CompactPolynomial, ConstantOne, KernelRangeError, KernelShapeError,
                           KroneckerDelta, ProductComposite, RConvolution, SquareExponential, kernel_from_spec)
 from .graphs import DEFAULT_STOP_PROB, LabeledGraph, ValidationReport, validate_graph
+from .graphio import PointCloud, spatial_graph, spatial_graphs
 from .gram import (GramResult, compute_gram, load_gram_binary, load_gram_csv, nodewise_gram, normalize_gram,
                    save_gram_binary, save_gram_csv, schedule_pairs, stream_nodewise)
 from .reorder import Permutation, apply_permutation, objective, partition_objective, pbr_reorder, pbr_reorder_many

@@ -15,7 +15,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libmgk.so"
-SOURCES = ["capi.cu", "tiles.cu", "pcg_warp.cu", "pcg_panel.cu", "pcg_block.cu", "pbr.cu", "bench_support.cu", "gram_post.cu"]
+SOURCES = ["capi.cu", "tiles.cu", "pcg_warp.cu", "pcg_panel.cu", "pcg_block.cu", "pbr.cu", "bench_support.cu", "gram_post.cu", "ingest.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -321,6 +321,9 @@ const char* mgk_version(void) { return "mgk-b200 0.1.0 (sm_100a)"; }
 
 const char* mgk_last_error(void) { return g_err.c_str(); }
 
+// error hook for the other translation units of the C-ABI (ingest.cu)
+int mgk_fail_ingest(int code, const char* msg) { return fail(code, "%s", msg); }
+
 int mgk_ctx_create(mgk_ctx** out, int device) {
   if (!out) return fail(MGK_E_INVALID, "null output pointer");
   int count = 0;

@@ -38,6 +38,7 @@ SIGNATURES = {
     "mgk_kernel": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int64, _P, _P, _P, _P, _P]),
     "mgk_gram_nodewise": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_int64, _P, _P, _P, _P]),
     "mgk_last_timing": (C.c_int, [_P, _P, _P]),
+    "mgk_spatial_edges": (C.c_int, [C.c_int, C.c_int32, _P, C.c_int, _P, C.c_double, _P, _P, _P, _P, _P]),
     "mgk_bench_peaks": (C.c_int, [C.c_int, _P, _P]),
     "mgk_transfer_bytes": (C.c_int, [_P, _P]),
 }
@@ -239,6 +240,28 @@ class Context:
         ms, n = C.c_double(), C.c_int32()
         check(self.lib.mgk_last_timing(self.h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+
+def spatial_edges(clouds, cutoff: float, device: int = 0):
+    """mgk_spatial_edges for a list of (n, dim) float64 point arrays -> per-cloud (ei, ej, w, d)."""
+    lib = load()
+    pts = [np.ascontiguousarray(np.asarray(p, dtype=np.float64)) for p in clouds]
+    dims = {p.shape[1] for p in pts if p.ndim == 2}
+    if any(p.ndim != 2 for p in pts) or len(dims) > 1:
+        raise ValueError("points must be (n, 2) or (n, 3) arrays of one dimension")
+    dim = dims.pop() if dims else 3
+    node_off = np.concatenate([[0], np.cumsum([len(p) for p in pts])]).astype(np.int64)
+    flat = np.ascontiguousarray(np.concatenate(pts).reshape(-1)) if pts else np.zeros(0)
+    eoff = np.empty(len(pts) + 1, dtype=np.int64)
+    check(lib.mgk_spatial_edges(int(device), len(pts), _ptr(node_off), dim, _ptr(flat), float(cutoff), _ptr(eoff),
+                                None, None, None, None))
+    ne = int(eoff[-1])
+    ei, ej = np.empty(ne, np.int32), np.empty(ne, np.int32)
+    w, d = np.empty(ne, np.float64), np.empty(ne, np.float64)
+    check(lib.mgk_spatial_edges(int(device), len(pts), _ptr(node_off), dim, _ptr(flat), float(cutoff), _ptr(eoff),
+                                _ptr(ei), _ptr(ej), _ptr(w), _ptr(d)))
+    return [(ei[eoff[k]:eoff[k + 1]], ej[eoff[k]:eoff[k + 1]], w[eoff[k]:eoff[k + 1]], d[eoff[k]:eoff[k + 1]])
+            for k in range(len(pts))]
 
 
 class PackedDataset:

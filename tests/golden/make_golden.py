@@ -1,6 +1,6 @@
 """Generate golden vectors by running the REAL reference (build container only).
 
-    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [composite]
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [composite|spatial]
 
 The reference (``mgksolver``, /root/reference/pkg/src) is imported read-only
 and evaluated on seeded inputs; inputs and outputs are written to
@@ -288,7 +288,28 @@ def make_composite():
     return out
 
 
+def make_spatial():
+    """Reference spatial_graph (graphio.py:211-240) on seeded point clouds (spatial.json)."""
+    from mgksolver.graphio import PointCloud, spatial_graph
+
+    rng = np.random.default_rng(211)
+    out = []
+    for n, dim, cutoff in ((1, 3, 2.0), (5, 2, 0.7), (40, 3, 0.45), (150, 3, 0.3), (90, 2, 0.2)):
+        pts = rng.random((n, dim)) * (1.0 + 0.3 * rng.random())
+        labels = rng.integers(0, 4, size=n)
+        g = spatial_graph(PointCloud(pts, labels), cutoff)
+        out.append({"points": pts.tolist(), "labels": labels.tolist(), "cutoff": cutoff,
+                    "ei": np.asarray(g.edges_i).tolist(), "ej": np.asarray(g.edges_j).tolist(),
+                    "w": np.asarray(g.weights).tolist(),
+                    "d": [] if g.edge_labels is None else np.asarray(g.edge_labels).reshape(-1).tolist()})
+    return out
+
+
 def main():
+    if sys.argv[1:] == ["spatial"]:
+        (HERE / "spatial.json").write_text(json.dumps(make_spatial()))
+        print("done")
+        return
     if sys.argv[1:] == ["composite"]:
         (HERE / "composite.json").write_text(json.dumps(make_composite()))
         print("done")

@@ -88,6 +88,36 @@ def test_composite_kernels_golden(mgk):
         assert np.max(np.abs(k.nodewise - nw)) <= REL * np.max(np.abs(nw)), rec["name"]
 
 
+def test_device_spatial_graph_bit_exact(mgk):
+    """Device spatial_graph (csrc/ingest.cu) == the reference's float64 numpy builder, bit for bit:
+    golden clouds (tests/golden/spatial.json) in one batch, and the config-2 molecule generator's clouds."""
+    from conftest import load_golden
+
+    recs = load_golden("spatial.json")
+    for cutoff in sorted({r["cutoff"] for r in recs}):
+        group = [r for r in recs if r["cutoff"] == cutoff]
+        dims = {len(r["points"][0]) for r in group}
+        for dim in dims:
+            sub = [r for r in group if len(r["points"][0]) == dim]
+            gs = mgk.spatial_graphs([mgk.PointCloud(np.asarray(r["points"]), np.asarray(r["labels"])) for r in sub],
+                                    cutoff)
+            for g, r in zip(gs, sub):
+                assert g.edges_i.tolist() == r["ei"] and g.edges_j.tolist() == r["ej"]
+                assert g.weights.tolist() == r["w"]
+                assert (g.edge_labels.reshape(-1).tolist() if g.edge_labels is not None else []) == r["d"]
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(3)
+    clouds = [synth.chain(rng, int(n), 1.4, 1.12) for n in (4, 17, 23, 60, 128)]
+    gs = mgk.spatial_graphs([mgk.PointCloud(c) for c in clouds], 3.0)
+    for c, g in zip(clouds, gs):
+        ei, ej, w, d = O.spatial_edges(c, 3.0)
+        assert g.edges_i.tolist() == ei.tolist() and g.edges_j.tolist() == ej.tolist()
+        assert g.weights.tolist() == w.tolist() and g.edge_labels.reshape(-1).tolist() == d.tolist()
+    with pytest.raises(ValueError, match="cutoff must be positive"):
+        mgk.spatial_graph(mgk.PointCloud(clouds[0]), 0.0)
+
+
 def test_closed_forms(mgk):
     a = mgk.LabeledGraph.from_edges(1, [], node_labels=np.array([0]), stop_prob=[0.3], start_prob=[1.0])
     b = mgk.LabeledGraph.from_edges(1, [], node_labels=np.array([1]), stop_prob=[0.3], start_prob=[1.0])

@@ -136,3 +136,13 @@ def test_schedule_golden(golden_gram):
     assert [list(p) for p in O.schedule_pairs([4, 4, 4], [6, 6, 6])] == s["uniform"]
     assert [list(p) for p in O.schedule_pairs([4, 100, 4, 4], [6, 2000, 6, 6])] == s["giant"]
     assert [list(p) for p in O.schedule_pairs([10, 20, 10, 7, 3], [30, 120, 20, 14, 2])] == s["mixed"]
+
+
+def test_spatial_edges_golden():
+    """graphio.spatial_graph (graphio.py:211-240) restated, bit-exact vs the reference on seeded clouds."""
+    from conftest import load_golden
+
+    for rec in load_golden("spatial.json"):
+        ei, ej, w, d = O.spatial_edges(rec["points"], rec["cutoff"])
+        assert ei.tolist() == rec["ei"] and ej.tolist() == rec["ej"]
+        assert w.tolist() == rec["w"] and d.tolist() == rec["d"]

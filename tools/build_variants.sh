@@ -12,7 +12,7 @@ while [ $# -ge 2 ]; do
   for f in capi pcg_panel; do $NVCC $FL $defs -c csrc/$f.cu -o build/$name/$f.o & done
   wait
   objs="build/$name/capi.o build/$name/pcg_panel.o"
-  for f in tiles pcg_warp pcg_block pbr bench_support gram_post; do objs="$objs build/$f.o"; done
+  for f in tiles pcg_warp pcg_block pbr bench_support gram_post ingest; do objs="$objs build/$f.o"; done
   $NVCC -gencode arch=compute_100a,code=sm_100a -shared -o libmgk_$name.so $objs -lcudart
   echo built libmgk_$name.so
 done
