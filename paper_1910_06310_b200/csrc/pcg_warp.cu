@@ -118,7 +118,7 @@ __device__ __noinline__ double diag_of(const DatasetDev& ds, const KernelDesc& v
 constexpr int kTinyMax = 128;
 
 template <int EK>
-__device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
+__device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
                            const GraphDesc& U, const GraphDesc& L, const float2* uwl, const int* uoff,
                            const int* urow, const float4* le, const int* lrow, double* P, double* AP, double* DG,
                            int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw,
@@ -515,7 +515,8 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       double pap = 0.0, pxp = 0.0;
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
-        if (i < nu && active) {
+        if (i >= nu) break;  // warp-uniform: no issue slots spent on absent rows
+        if (active) {
           const float p = S.P[i][lane];
           const float ap = fmaf(dv[i], p, -S.OFF[i][lane]);
           S.OFF[i][lane] = ap;
@@ -531,7 +532,8 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       double rr_l = 0.0, rz_l = 0.0;
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
-        if (i < nu && active) {
+        if (i >= nu) break;  // warp-uniform: no issue slots spent on absent rows
+        if (active) {
           if constexpr (NODEWISE) S.X[i][lane] = fmaf(af, S.P[i][lane], S.X[i][lane]);
           const float r = fmaf(-af, S.OFF[i][lane], rv[i]);
           const float z = r * rcp_approx(dv[i]);
