@@ -1,9 +1,11 @@
 // Device graph ingestion: the spatial_graph cutoff builder
 // (graphio.py:211-240) for a batch of point clouds.  Pairs i < j closer than
 // the cutoff become edges in (i, j) lexicographic order with
-// w = (1 - (d / cutoff)^2)^2 and label d, bit-identical to the reference's
-// float64 numpy evaluation: d = sqrt((dx*dx + dy*dy) + dz*dz) with every
-// operation rounded separately (no FMA contraction, explicit _rn intrinsics).
+// w = (1 - (d / cutoff)^2)^2 and label d.  Edges and d are bit-identical to the
+// reference's float64 numpy evaluation, d = sqrt((dx*dx + dy*dy) + dz*dz) with
+// every operation rounded separately (no FMA contraction, explicit _rn
+// intrinsics); w uses correctly rounded squares, within 1 ulp of numpy's
+// scalar ``** 2`` (libm pow, not correctly rounded).
 //
 //   k_spatial_rows  warp per point (row i): ballot-count of j > i in range
 //   host scan       row starts
