@@ -135,7 +135,7 @@ int mgk_kernel(mgk_ctx* ctx, int32_t a, int32_t b, double tol, int64_t max_iter,
  * into points[sum n * dim] (dim 2 or 3, float64, row-major).  Every pair i < j
  * with distance d < cutoff becomes an edge (i, j lexicographic, local ids),
  * w = (1 - (d/cutoff)^2)^2, label d -- edges and d bit-identical to the
- * reference's float64 numpy evaluation, w within 1 ulp (numpy squares with libm pow).  Writes edge_off[N+1]; call with the four edge arrays NULL
+ * reference's float64 numpy evaluation, w within 1e-13 relative (numpy squares with libm pow).  Writes edge_off[N+1]; call with the four edge arrays NULL
  * to size them, then again with buffers of edge_off[N] entries. */
 int mgk_spatial_edges(int device, int32_t N, const int64_t* node_off, int dim, const double* points, double cutoff,
                       int64_t* edge_off, int32_t* ei, int32_t* ej, double* w, double* d);

@@ -4,8 +4,8 @@
 // w = (1 - (d / cutoff)^2)^2 and label d.  Edges and d are bit-identical to the
 // reference's float64 numpy evaluation, d = sqrt((dx*dx + dy*dy) + dz*dz) with
 // every operation rounded separately (no FMA contraction, explicit _rn
-// intrinsics); w uses correctly rounded squares, within 1 ulp of numpy's
-// scalar ``** 2`` (libm pow, not correctly rounded).
+// intrinsics); w uses correctly rounded squares, within 1e-13 of numpy's
+// scalar ``** 2`` (libm pow, not correctly rounded; 1 - t^2 amplifies its ulp).
 //
 //   k_spatial_rows  warp per point (row i): ballot-count of j > i in range
 //   host scan       row starts

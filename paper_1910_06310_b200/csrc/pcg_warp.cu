@@ -118,7 +118,7 @@ __device__ __noinline__ double diag_of(const DatasetDev& ds, const KernelDesc& v
 constexpr int kTinyMax = 128;
 
 template <int EK>
-__device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
+__device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
                            const GraphDesc& U, const GraphDesc& L, const float2* uwl, const int* uoff,
                            const int* urow, const float4* le, const int* lrow, double* P, double* AP, double* DG,
                            int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw,
