@@ -15,7 +15,11 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libmgk.so"
-SOURCES = ["capi.cu", "tiles.cu", "pcg_warp.cu", "pcg_panel.cu", "pcg_block.cu", "pbr.cu", "bench_support.cu", "gram_post.cu", "ingest.cu"]
+SOURCES = ["capi.cu", "tiles.cu", "pcg_warp.cu", "pcg_panel.cu", "pcg_block.cu", "pbr.cu", "bench_support.cu",
+           "gram_post.cu", "ingest.cu"]
+# sources compiled more than once: (source, object stem, extra flags)
+VARIANTS = {"pcg_panel.cu": [("pcg_panel_256", ["-DMGK_PANEL_THREADS=256", "-DMGK_PANEL_NS=p256"]),
+                             ("pcg_panel_512", ["-DMGK_PANEL_THREADS=512", "-DMGK_PANEL_NS=p512"])]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -38,10 +42,11 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         common += ["-Xptxas", "-v"]
     procs = []
     for s in srcs:
-        o = objdir / (s.stem + ".o")
-        objs.append(o)
-        procs.append((s, subprocess.Popen(common + ["-c", str(s), "-o", str(o)], stdout=subprocess.PIPE,
-                                          stderr=subprocess.STDOUT, text=True)))
+        for stem, extra in VARIANTS.get(s.name, [(s.stem, [])]):
+            o = objdir / (stem + ".o")
+            objs.append(o)
+            procs.append((s, subprocess.Popen(common + extra + ["-c", str(s), "-o", str(o)], stdout=subprocess.PIPE,
+                                              stderr=subprocess.STDOUT, text=True)))
     for s, p in procs:
         out, _ = p.communicate()
         if verbose or p.returncode:

@@ -754,6 +754,8 @@ static bool panel_dataset(const mgk_ctx* c) {
 
 // Largest n*m the panel solver keeps in shared memory (P and Ap: 2 n m floats).
 constexpr int64_t kPanelSmemNM = 8192;
+// Jobs whose largest pair reaches this n*m run the 512-thread panel CTAs.
+constexpr int64_t kPanelWideNM = 32768;
 // Graphs with at least large_n() nodes pair with each other on the whole device
 // (grid class); explicit pair lists use n*m >= large_n()^2.  MGK_GRID_N
 // overrides the threshold (tests drive the grid path at oracle-sized graphs).
@@ -782,6 +784,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   // scratch slabs (block and panel jobs run one after another on the stream and share the buffer)
   std::vector<int64_t> slabs(jobs.size(), 0);
   std::vector<int> ctas(jobs.size(), 0), svec(jobs.size(), 0);
+  std::vector<char> big(jobs.size(), 0);
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   const int64_t budget = (int64_t)(free_b * 0.6) / 4 + (int64_t)c->d_scratch.n;
@@ -799,7 +802,10 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
       // and the whole L1 stays available to the gathers
       const int64_t smem_nm = getenv("MGK_PANEL_SMEM_NM") ? atoll(getenv("MGK_PANEL_SMEM_NM")) : kPanelSmemNM;
       svec[k] = nm <= smem_nm ? (int)(2 * nm) : 0;
-      int per_sm = panel_ctas_per_sm(svec[k]);
+      // large pairs (P streamed through L2): one 512-thread CTA per SM keeps the resident P
+      // vectors within L2; mid-size pairs: two 256-thread CTAs per SM
+      big[k] = svec[k] == 0 && nm >= kPanelWideNM && !getenv("MGK_PANEL_NO512");
+      int per_sm = big[k] ? p512::panel_ctas_per_sm(0) : p256::panel_ctas_per_sm(svec[k]);
       if (const char* e = getenv("MGK_PANEL_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
       ctas[k] = per_sm * c->num_sms;
     } else {
@@ -811,7 +817,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   }
   if (need > 0) CUDA_TRY(c->d_scratch.alloc((size_t)need));
   int64_t grid_vstride = 0;
-  const int gblocks = grid_blocks(c->num_sms);
+  const int gblocks = p256::grid_blocks(c->num_sms);
   for (auto& j : jobs)
     if (j.kernel == JK_GRID && j.job.npairs > 0) grid_vstride = std::max(grid_vstride, (j.max_n * j.max_m + 31) / 32 * 32);
   if (grid_vstride > 0) {
@@ -859,11 +865,11 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     else if (j.kernel == JK_TINY)
       e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, js);
     else if (j.kernel == JK_GRID)
-      e = launch_pcg_grid(c->ds, c->vk, c->ek, j.job, prm, o, c->d_gridvec.ptr, grid_vstride, c->d_gridbuf.ptr,
+      e = p256::launch_pcg_grid(c->ds, c->vk, c->ek, j.job, prm, o, c->d_gridvec.ptr, grid_vstride, c->d_gridbuf.ptr,
                           gblocks, s);
     else if (j.kernel == JK_PANEL)
-      e = launch_pcg_panel(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slabs[k],
-                           ctas[k], svec[k], s);
+      e = (big[k] ? p512::launch_pcg_panel : p256::launch_pcg_panel)(
+          c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slabs[k], ctas[k], svec[k], s);
     else
       e = launch_pcg_block(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->d_scratch.ptr, slabs[k],
                            ctas[k], s);

@@ -131,17 +131,24 @@ cudaError_t launch_pcg_warp(const DatasetDev& ds, const KernelDesc& vk, const Ke
 cudaError_t launch_pcg_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                             int num_sms, cudaStream_t stream);
-// panel class (pcg_panel.cu): CTA per pair, any size whose lane graph has row panels
-cudaError_t launch_pcg_panel(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
-                             const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
-                             float* scratch, int64_t scratch_floats_per_cta, int nctas, int smem_vec_floats,
-                             cudaStream_t stream);
-int panel_ctas_per_sm(int smem_vec_floats);
-// grid class (pcg_panel.cu): one pair at a time on the whole device (cooperative launch)
-cudaError_t launch_pcg_grid(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
-                            const SolveParams& prm, const SolveOut& out, float* vec, int64_t vstride, double2* gbuf,
-                            int nblocks, cudaStream_t stream);
-int grid_blocks(int num_sms);
+// panel and grid classes (pcg_panel.cu, built as p256 and p512: 256- / 512-thread CTAs)
+#define MGK_PANEL_DECLS                                                                                    \
+  cudaError_t launch_pcg_panel(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,         \
+                               const PairJob& job, const SolveParams& prm, const SolveOut& out,          \
+                               unsigned long long* queue, float* scratch, int64_t scratch_floats_per_cta, \
+                               int nctas, int smem_vec_floats, cudaStream_t stream);                     \
+  int panel_ctas_per_sm(int smem_vec_floats);                                                            \
+  cudaError_t launch_pcg_grid(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,          \
+                              const PairJob& job, const SolveParams& prm, const SolveOut& out, float* vec,  \
+                              int64_t vstride, double2* gbuf, int nblocks, cudaStream_t stream);         \
+  int grid_blocks(int num_sms);
+namespace p256 {
+MGK_PANEL_DECLS
+}
+namespace p512 {
+MGK_PANEL_DECLS
+}
+#undef MGK_PANEL_DECLS
 // Gram post-processing (gram_post.cu)
 cudaError_t launch_gram_normalize(double* K, int64_t G, double* diag, int* bad, int num_sms, cudaStream_t stream,
                                   bool* nonpositive);

@@ -30,6 +30,13 @@
 
 namespace mgk {
 
+// This file is compiled twice: CTAs of 256 threads (namespace p256: mid-size pairs, two CTAs per SM)
+// and of 512 threads (p512: large pairs, one CTA per SM so the resident P vectors stay in L2).
+#ifndef MGK_PANEL_NS
+#define MGK_PANEL_NS p256
+#endif
+namespace MGK_PANEL_NS {
+
 namespace cg = cooperative_groups;
 
 #ifndef MGK_PANEL_THREADS
@@ -1006,4 +1013,5 @@ cudaError_t launch_pcg_grid(const DatasetDev& ds, const KernelDesc& vk, const Ke
   return launch_grid_nw<false>(ds, vk, ek, job, prm, out, vec, vstride, gbuf, nblocks, stream);
 }
 
+}  // namespace MGK_PANEL_NS
 }  // namespace mgk
