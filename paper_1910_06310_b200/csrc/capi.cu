@@ -817,7 +817,8 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   }
   if (need > 0) CUDA_TRY(c->d_scratch.alloc((size_t)need));
   int64_t grid_vstride = 0;
-  const int gblocks = p256::grid_blocks(c->num_sms);
+  const bool grid512 = getenv("MGK_GRID256") == nullptr;
+  const int gblocks = grid512 ? p512::grid_blocks(c->num_sms) : p256::grid_blocks(c->num_sms);
   for (auto& j : jobs)
     if (j.kernel == JK_GRID && j.job.npairs > 0) grid_vstride = std::max(grid_vstride, (j.max_n * j.max_m + 31) / 32 * 32);
   if (grid_vstride > 0) {
@@ -865,7 +866,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     else if (j.kernel == JK_TINY)
       e = launch_pcg_tiny(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, js);
     else if (j.kernel == JK_GRID)
-      e = p256::launch_pcg_grid(c->ds, c->vk, c->ek, j.job, prm, o, c->d_gridvec.ptr, grid_vstride, c->d_gridbuf.ptr,
+      e = (grid512 ? p512::launch_pcg_grid : p256::launch_pcg_grid)(c->ds, c->vk, c->ek, j.job, prm, o, c->d_gridvec.ptr, grid_vstride, c->d_gridbuf.ptr,
                           gblocks, s);
     else if (j.kernel == JK_PANEL)
       e = (big[k] ? p512::launch_pcg_panel : p256::launch_pcg_panel)(
