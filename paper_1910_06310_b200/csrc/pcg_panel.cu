@@ -70,66 +70,6 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
   return s;
 }
 
-#ifndef MGK_PANEL_PIPELINE
-#define MGK_PANEL_PIPELINE 0
-#endif
-#if MGK_PANEL_PIPELINE
-// acc[t] += sum_{k in [k0, k1)} kappa(e_k, e'_t) w_k P[j_k][lcol[t]]   (U row, warp-uniform)
-//
-// P lives in L1/L2 (or shared memory), so the gathers are latency-bound: the
-// loop is software-pipelined over batches of two U nonzeros -- row entries two
-// batches ahead, gathers one batch ahead -- so each warp keeps 2 x NS gathers
-// in flight while it evaluates the edge kernel of the current batch.  Padding
-// entries have weight 0 and point at row 0 (a valid address).
-template <int NS, int EK>
-__device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float4* __restrict__ ue, int k0, int k1,
-                                               const float* P, int m, const int (&lcol)[NS],
-                                               const float (&llab)[NS], float (&acc)[NS]) {
-  if (k0 >= k1) return;
-  auto entry = [&](int k) {
-    return k < k1 ? ue[k] : make_float4(__int_as_float(0), 0.0f, 0.0f, 0.0f);
-  };
-  float4 e0 = entry(k0), e1 = entry(k0 + 1);
-  float4 f0 = entry(k0 + 2), f1 = entry(k0 + 3);
-  float p0[NS], p1[NS];
-  {
-    const float* r0 = P + __float_as_int(e0.x) * m;
-    const float* r1 = P + __float_as_int(e1.x) * m;
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      p0[t] = r0[lcol[t]];
-      p1[t] = r1[lcol[t]];
-    }
-  }
-  for (int k = k0; k < k1; k += 2) {
-    // issue the next batch's gathers and the entries of the batch after it
-    const float* s0 = P + __float_as_int(f0.x) * m;
-    const float* s1 = P + __float_as_int(f1.x) * m;
-    float q0[NS], q1[NS];
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      q0[t] = s0[lcol[t]];
-      q1[t] = s1[lcol[t]];
-    }
-    const float4 g0 = entry(k + 4), g1 = entry(k + 5);
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y), p0[t], acc[t]);
-      acc[t] = fmaf(edge_kappa_w<EK>(ek, e1.z, llab[t], EK == KK_SE ? e1.w : e1.y), p1[t], acc[t]);
-    }
-    e0 = f0;
-    e1 = f1;
-    f0 = g0;
-    f1 = g1;
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      p0[t] = q0[t];
-      p1[t] = q1[t];
-    }
-  }
-}
-
-#else
 // acc[t] += sum_{k in [k0, k1)} kappa(e_k, e'_t) w_k P[j_k][lcol[t]]   (U row, warp-uniform)
 template <int NS, int EK>
 __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float4* __restrict__ ue, int k0, int k1,
@@ -161,7 +101,6 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
   }
 }
 
-#endif
 
 struct PairView {
   const int32_t* urp;   // U row pointers (relative to ue)
