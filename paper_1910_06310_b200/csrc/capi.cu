@@ -833,7 +833,6 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   // other's tails.  MGK_SERIAL=1 runs everything on the main stream.
   // The cooperative grid jobs go first and alone (their blocks must all be resident).
   const bool serial = getenv("MGK_SERIAL") != nullptr;
-  bool used[2] = {false, false};
   std::vector<size_t> order;
   for (size_t k = 0; k < jobs.size(); ++k)
     if (jobs[k].kernel == JK_GRID) order.push_back(k);
@@ -860,7 +859,6 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     cudaError_t e;
     const int q = serial ? -1 : (j.kernel == JK_WARP ? 0 : (j.kernel == JK_TINY ? 1 : -1));
     cudaStream_t js = q < 0 ? s : c->side[q];
-    if (q >= 0) used[q] = true;
     if (j.kernel == JK_WARP)
       e = launch_pcg_warp(c->ds, c->vk, c->ek, j.job, prm, o, c->d_queue.ptr + k, c->num_sms, j.slots, js);
     else if (j.kernel == JK_TINY)
@@ -885,7 +883,6 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     CUDA_TRY(cudaEventRecord(c->evside[q], c->side[q]));
     CUDA_TRY(cudaStreamWaitEvent(s, c->evside[q], 0));
   }
-  (void)used;
   CUDA_TRY(cudaEventRecord(e1, s));
   if (!sync) return MGK_OK;
   CUDA_TRY(cudaEventSynchronize(e1));
