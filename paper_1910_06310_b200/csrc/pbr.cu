@@ -30,6 +30,8 @@ constexpr int kMaxPasses = 10;
 constexpr int kNPMax = 128;  // distinct neighbour parts tracked per node in a gain evaluation
 constexpr int kLogMax = 512;
 __device__ int g_pbr_log[1 + 4 * kLogMax];  // debug: first FM moves of block 0 (u, dst, gain, pass)
+// profile: SM cycles of the slowest graph's phases (max over graphs): bisection, K-way FM, rest
+__device__ unsigned long long g_pbr_cycles[3];
 
 struct PbrScratch {
   int* rowptr;   // n + 1
@@ -661,10 +663,17 @@ __global__ void __launch_bounds__(kPbrThreads) k_pbr(const PbrGraph* __restrict_
       }
       __syncthreads();
       int* cp = s.cand + (int64_t)c * n;
+      const long long c0 = clock64();
       recursive_parts(s, n, k, cp, red64, redll, shw, &shc, &shi);
       for (int i = threadIdx.x; i < n; i += blockDim.x) s.dbg[(int64_t)c * n + i] = cp[i];
       __syncthreads();
+      const long long c1 = clock64();
       ok &= fm_refine(s, n, k, cp, red64, redll, &shflag);
+      const long long c2 = clock64();
+      if (threadIdx.x == 0) {
+        atomicMax(&g_pbr_cycles[0], (unsigned long long)(c1 - c0));
+        atomicMax(&g_pbr_cycles[1], (unsigned long long)(c2 - c1));
+      }
     }
     if (!ok && threadIdx.x == 0) atomicExch(status, 1);
     const long long o0 = pair_count(s, n, k, s.cand, false, redll);
@@ -760,6 +769,11 @@ int pbr_device(int G, const std::vector<int64_t>& node_off, const std::vector<in
     e = cudaMemcpyAsync(forward.data(), d_fwd, sizeof(int64_t) * nn, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess && getenv("MGK_PBR_PROFILE")) {
+    unsigned long long cyc[3] = {0, 0, 0};
+    cudaMemcpyFromSymbol(cyc, g_pbr_cycles, sizeof(cyc));
+    fprintf(stderr, "PBRPROF max cycles per candidate: bisection %llu, fm %llu\n", cyc[0], cyc[1]);
+  }
   if (e == cudaSuccess && getenv("MGK_PBR_DEBUG")) {  // candidate partitions of every graph, for parity triage
     for (int g = 0; g < G; ++g) {
       if (gs[g].k <= 1 || gs[g].S == 0) continue;
