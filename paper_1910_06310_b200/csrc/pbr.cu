@@ -51,6 +51,10 @@ struct PbrScratch {
   int* targets;  // k
   unsigned* adjbits;  // k x W   bit Q of row P: ec[P][Q] > 0 (P != Q), W = ceil(k / 32)
   unsigned* elig;     // W       destination parts allowed for the current move
+  unsigned long long* kcache;  // n   balanced-state best-move key of every node (FM key cache)
+  int* kvalid;        // n       cache entry still exact
+  unsigned* pmask;    // W       parts touched by the last move (cache invalidation)
+  int* flip;          // 1       an adjacency bit flipped during the last move
   int* stack;    // 6k   recursion tasks (begin, end, first_part, nparts)
   int* dbg;      // 2n   candidates before FM refinement (parity triage)
 };
@@ -59,7 +63,8 @@ __host__ __device__ inline int pbr_words(int k) { return (k + 31) >> 5; }
 
 __host__ __device__ inline int64_t pbr_scratch_ints(int n, int S, int k) {
   return (int64_t)(n + 1) + S + n + 2 * n + n + n + n + n + 2 * n + n + 4 * n + (int64_t)n * k + (int64_t)k * k + k +
-         k + (int64_t)k * pbr_words(k) + pbr_words(k) + 6 * (int64_t)k + 2 * (int64_t)n + 64;
+         k + (int64_t)k * pbr_words(k) + pbr_words(k) + (2 * (int64_t)n + 2) + n + pbr_words(k) + 1 +
+         6 * (int64_t)k + 2 * (int64_t)n + 64;
 }
 
 __device__ PbrScratch carve(int* base, int n, int S, int k) {
@@ -82,6 +87,11 @@ __device__ PbrScratch carve(int* base, int n, int S, int k) {
   s.targets = p; p += k;
   s.adjbits = reinterpret_cast<unsigned*>(p); p += (int64_t)k * pbr_words(k);
   s.elig = reinterpret_cast<unsigned*>(p); p += pbr_words(k);
+  if ((p - base) & 1) ++p;  // 8-byte alignment of the key cache
+  s.kcache = reinterpret_cast<unsigned long long*>(p); p += 2 * (int64_t)n;
+  s.kvalid = p; p += n;
+  s.pmask = reinterpret_cast<unsigned*>(p); p += pbr_words(k);
+  s.flip = p; p += 1;
   s.stack = p;
   p += 6 * k;
   s.dbg = p;
@@ -329,15 +339,15 @@ __device__ long long ec_objective(const PbrScratch& s, int k, long long* redll) 
 }
 
 // adjacency bit (P, Q) <- ec[P][Q] > 0 (diagonal never stored; it never enters a gain)
-__device__ __forceinline__ void sync_adjbit(const PbrScratch& s, int k, int P, int Q) {
-  if (P == Q) return;
+__device__ __forceinline__ bool sync_adjbit(const PbrScratch& s, int k, int P, int Q) {
+  if (P == Q) return false;
   const unsigned bit = 1u << (Q & 31);
   unsigned* wp = s.adjbits + (int64_t)P * pbr_words(k) + (Q >> 5);
-  if (s.ec[(int64_t)P * k + Q] > 0)
-    atomicOr(wp, bit);
-  else
-    atomicAnd(wp, ~bit);
+  if (s.ec[(int64_t)P * k + Q] > 0) return !(atomicOr(wp, bit) & bit);
+  return (atomicAnd(wp, ~bit) & bit) != 0;
 }
+
+__device__ __forceinline__ void mark_part(const PbrScratch& s, int P) { atomicOr(&s.pmask[P >> 5], 1u << (P & 31)); }
 
 __device__ void fm_move(PbrScratch& s, int k, int u, int dst) {
   const int src = s.parts[u];
@@ -352,15 +362,40 @@ __device__ void fm_move(PbrScratch& s, int k, int u, int dst) {
     atomicAdd(&s.conn[(int64_t)v * k + dst], 1);
   }
   __syncthreads();
+  bool flipped = false;
   for (int q = s.rowptr[u] + threadIdx.x; q < s.rowptr[u + 1]; q += blockDim.x) {
-    const int p = s.parts[s.adj[q]];
-    sync_adjbit(s, k, src, p);
-    sync_adjbit(s, k, p, src);
-    sync_adjbit(s, k, dst, p);
-    sync_adjbit(s, k, p, dst);
+    const int v = s.adj[q];
+    const int p = s.parts[v];
+    flipped |= sync_adjbit(s, k, src, p);
+    flipped |= sync_adjbit(s, k, p, src);
+    flipped |= sync_adjbit(s, k, dst, p);
+    flipped |= sync_adjbit(s, k, p, dst);
+    // key-cache invalidation: v's conn row and neighbour parts changed; part p's ec row changed
+    s.kvalid[v] = 0;
+    mark_part(s, p);
+  }
+  if (flipped) *s.flip = 1;
+  if (threadIdx.x == 0) {
+    s.kvalid[u] = 0;
+    mark_part(s, src);
+    mark_part(s, dst);
   }
   __syncthreads();
   if (threadIdx.x == 0) s.parts[u] = dst;
+  __syncthreads();
+}
+
+// Drop the cached keys the last move(s) may have changed: nodes of marked parts (their part's ec row
+// changed) and, if an adjacency bit flipped, every node.  Clears the marks.
+__device__ void invalidate_marked(PbrScratch& s, int n, int k) {
+  const bool all = *s.flip != 0;
+  for (int w = threadIdx.x; w < n; w += blockDim.x) {
+    const int P = s.parts[w];
+    if (all || ((s.pmask[P >> 5] >> (P & 31)) & 1u)) s.kvalid[w] = 0;
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < pbr_words(k); w += blockDim.x) s.pmask[w] = 0;
+  if (threadIdx.x == 0) *s.flip = 0;
   __syncthreads();
 }
 
@@ -475,6 +510,8 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
     }
     s.adjbits[x] = word;
   }
+  for (int w = threadIdx.x; w < W; w += blockDim.x) s.pmask[w] = 0;
+  if (threadIdx.x == 0) *s.flip = 0;
   __syncthreads();
   for (int pass = 0; pass < kMaxPasses; ++pass) {
     for (int p = threadIdx.x; p < k; p += blockDim.x) s.sizes[p] = 0;
@@ -482,6 +519,7 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       atomicAdd(&s.sizes[s.parts[i]], 1);
       s.locked[i] = 0;
+      s.kvalid[i] = 0;
     }
     __syncthreads();
     long long badl = 0;
@@ -511,9 +549,20 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
         if (balanced && ignore_locks) break;  // the lock-free fallback only applies when unbalanced
         for (int u = threadIdx.x; u < n; u += blockDim.x) {
           if (!ignore_locks && s.locked[u]) continue;
-          const int A = s.parts[u];
-          if (!balanced && !(s.sizes[A] > s.targets[A])) continue;
-          const unsigned long long kk = fm_node_key(s, k, u);
+          unsigned long long kk;
+          if (balanced) {
+            // every destination allowed: the node's best move only changes when a move touched its
+            // conn row, its part's ec row or an adjacency bit, so cached keys stay exact otherwise
+            if (!s.kvalid[u]) {
+              s.kcache[u] = fm_node_key(s, k, u);
+              s.kvalid[u] = 1;
+            }
+            kk = s.kcache[u];
+          } else {
+            const int A = s.parts[u];
+            if (!(s.sizes[A] > s.targets[A])) continue;
+            kk = fm_node_key(s, k, u);
+          }
           key = kk > key ? kk : key;
         }
         key = block_max_u64(key, red64);
@@ -525,6 +574,7 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
       const int src = s.parts[u];
       __syncthreads();
       fm_move(s, k, u, dst);
+      invalidate_marked(s, n, k);
       if (threadIdx.x == 0) {
         s.sizes[src] -= 1;
         s.sizes[dst] += 1;
