@@ -27,7 +27,6 @@ namespace mgk {
 constexpr int kPbrThreads = 512;
 constexpr int kPbrWarps = kPbrThreads / 32;
 constexpr int kMaxPasses = 10;
-constexpr int kNPMax = 128;  // distinct neighbour parts tracked per node in a gain evaluation
 constexpr int kLogMax = 512;
 __device__ int g_pbr_log[1 + 4 * kLogMax];  // debug: first FM moves of block 0 (u, dst, gain, pass)
 // profile: SM cycles of the slowest graph's phases (max over graphs): bisection, K-way FM, rest
@@ -54,6 +53,10 @@ struct PbrScratch {
   unsigned long long* kcache;  // n   balanced-state best-move key of every node (FM key cache)
   int* kvalid;        // n       cache entry still exact
   unsigned* pmask;    // W       parts touched by the last move (cache invalidation)
+  unsigned* fmask;    // W       parts whose adjacency-bit row flipped during the last move
+  int* npl;           // S       per node: the distinct parts of its neighbours (capacity = degree,
+                      //         laid out like adj), maintained incrementally by every move
+  int* npc;           // n       their count
   int* flip;          // 1       an adjacency bit flipped during the last move
   int* stack;    // 6k   recursion tasks (begin, end, first_part, nparts)
   int* dbg;      // 2n   candidates before FM refinement (parity triage)
@@ -63,7 +66,7 @@ __host__ __device__ inline int pbr_words(int k) { return (k + 31) >> 5; }
 
 __host__ __device__ inline int64_t pbr_scratch_ints(int n, int S, int k) {
   return (int64_t)(n + 1) + S + n + 2 * n + n + n + n + n + 2 * n + n + 4 * n + (int64_t)n * k + (int64_t)k * k + k +
-         k + (int64_t)k * pbr_words(k) + pbr_words(k) + (2 * (int64_t)n + 2) + n + pbr_words(k) + 1 +
+         k + (int64_t)k * pbr_words(k) + pbr_words(k) + (2 * (int64_t)n + 2) + n + 2 * pbr_words(k) + 1 + S + n +
          6 * (int64_t)k + 2 * (int64_t)n + 64;
 }
 
@@ -91,7 +94,10 @@ __device__ PbrScratch carve(int* base, int n, int S, int k) {
   s.kcache = reinterpret_cast<unsigned long long*>(p); p += 2 * (int64_t)n;
   s.kvalid = p; p += n;
   s.pmask = reinterpret_cast<unsigned*>(p); p += pbr_words(k);
+  s.fmask = reinterpret_cast<unsigned*>(p); p += pbr_words(k);
   s.flip = p; p += 1;
+  s.npl = p; p += S;
+  s.npc = p; p += n;
   s.stack = p;
   p += 6 * k;
   s.dbg = p;
@@ -348,6 +354,10 @@ __device__ __forceinline__ bool sync_adjbit(const PbrScratch& s, int k, int P, i
 }
 
 __device__ __forceinline__ void mark_part(const PbrScratch& s, int P) { atomicOr(&s.pmask[P >> 5], 1u << (P & 31)); }
+__device__ __forceinline__ void mark_flip(const PbrScratch& s, int P) {
+  atomicOr(&s.fmask[P >> 5], 1u << (P & 31));
+  *s.flip = 1;
+}
 
 __device__ void fm_move(PbrScratch& s, int k, int u, int dst) {
   const int src = s.parts[u];
@@ -358,23 +368,34 @@ __device__ void fm_move(PbrScratch& s, int k, int u, int dst) {
     atomicSub(&s.ec[(int64_t)p * k + src], 1);
     atomicAdd(&s.ec[(int64_t)dst * k + p], 1);
     atomicAdd(&s.ec[(int64_t)p * k + dst], 1);
-    atomicSub(&s.conn[(int64_t)v * k + src], 1);
-    atomicAdd(&s.conn[(int64_t)v * k + dst], 1);
+    const int was_src = atomicSub(&s.conn[(int64_t)v * k + src], 1);
+    const int was_dst = atomicAdd(&s.conn[(int64_t)v * k + dst], 1);
+    // v's neighbour-part set: src leaves when its last link goes, dst joins with the first
+    // (each v occurs once in u's adjacency, so one thread owns v's list here)
+    int* l = s.npl + s.rowptr[v];
+    if (was_src == 1) {
+      const int c = s.npc[v];
+      for (int t = 0; t < c; ++t)
+        if (l[t] == src) {
+          l[t] = l[c - 1];
+          break;
+        }
+      s.npc[v] = c - 1;
+    }
+    if (was_dst == 0) l[s.npc[v]++] = dst;
   }
   __syncthreads();
-  bool flipped = false;
   for (int q = s.rowptr[u] + threadIdx.x; q < s.rowptr[u + 1]; q += blockDim.x) {
     const int v = s.adj[q];
     const int p = s.parts[v];
-    flipped |= sync_adjbit(s, k, src, p);
-    flipped |= sync_adjbit(s, k, p, src);
-    flipped |= sync_adjbit(s, k, dst, p);
-    flipped |= sync_adjbit(s, k, p, dst);
+    if (sync_adjbit(s, k, src, p)) mark_flip(s, src);
+    if (sync_adjbit(s, k, p, src)) mark_flip(s, p);
+    if (sync_adjbit(s, k, dst, p)) mark_flip(s, dst);
+    if (sync_adjbit(s, k, p, dst)) mark_flip(s, p);
     // key-cache invalidation: v's conn row and neighbour parts changed; part p's ec row changed
     s.kvalid[v] = 0;
     mark_part(s, p);
   }
-  if (flipped) *s.flip = 1;
   if (threadIdx.x == 0) {
     s.kvalid[u] = 0;
     mark_part(s, src);
@@ -385,16 +406,22 @@ __device__ void fm_move(PbrScratch& s, int k, int u, int dst) {
   __syncthreads();
 }
 
-// Drop the cached keys the last move(s) may have changed: nodes of marked parts (their part's ec row
-// changed) and, if an adjacency bit flipped, every node.  Clears the marks.
+// Drop the cached keys the last move may have changed: nodes of marked parts (their part's ec row
+// changed) and, for every part whose adjacency-bit row flipped, the neighbours of its members (the
+// nodes with that part in NP).  Clears the marks.
 __device__ void invalidate_marked(PbrScratch& s, int n, int k) {
-  const bool all = *s.flip != 0;
+  const bool any_flip = *s.flip != 0;
   for (int w = threadIdx.x; w < n; w += blockDim.x) {
     const int P = s.parts[w];
-    if (all || ((s.pmask[P >> 5] >> (P & 31)) & 1u)) s.kvalid[w] = 0;
+    if ((s.pmask[P >> 5] >> (P & 31)) & 1u) s.kvalid[w] = 0;
+    if (any_flip && ((s.fmask[P >> 5] >> (P & 31)) & 1u))
+      for (int q = s.rowptr[w]; q < s.rowptr[w + 1]; ++q) s.kvalid[s.adj[q]] = 0;
   }
   __syncthreads();
-  for (int w = threadIdx.x; w < pbr_words(k); w += blockDim.x) s.pmask[w] = 0;
+  for (int w = threadIdx.x; w < pbr_words(k); w += blockDim.x) {
+    s.pmask[w] = 0;
+    s.fmask[w] = 0;
+  }
   if (threadIdx.x == 0) *s.flip = 0;
   __syncthreads();
 }
@@ -418,14 +445,8 @@ __device__ unsigned long long fm_node_key(const PbrScratch& s, int k, int u) {
   const int A = s.parts[u];
   const int* cu = s.conn + (int64_t)u * k;
   const int* ecA = s.ec + (int64_t)A * k;
-  int np[kNPMax];
-  int nnp = 0;
-  for (int q = s.rowptr[u]; q < s.rowptr[u + 1]; ++q) {
-    const int P = s.parts[s.adj[q]];
-    bool seen = false;
-    for (int t = 0; t < nnp; ++t) seen |= (np[t] == P);
-    if (!seen && nnp < kNPMax) np[nnp++] = P;
-  }
+  const int* np = s.npl + s.rowptr[u];  // distinct neighbour parts (order irrelevant below)
+  const int nnp = s.npc[u];
   int L = 0;
   for (int t = 0; t < nnp; ++t) {
     const int P = np[t];
@@ -500,6 +521,17 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
     }
   }
   __syncthreads();
+  for (int u = threadIdx.x; u < n; u += blockDim.x) {
+    int* l = s.npl + s.rowptr[u];
+    int c = 0;
+    for (int q = s.rowptr[u]; q < s.rowptr[u + 1]; ++q) {
+      const int P = s.parts[s.adj[q]];
+      bool seen = false;
+      for (int t = 0; t < c; ++t) seen |= (l[t] == P);
+      if (!seen) l[c++] = P;
+    }
+    s.npc[u] = c;
+  }
   const int W = pbr_words(k);
   for (int64_t x = threadIdx.x; x < (int64_t)k * W; x += blockDim.x) {
     const int P = (int)(x / W), w = (int)(x - (int64_t)P * W);
@@ -510,7 +542,10 @@ __device__ bool fm_refine(PbrScratch& s, int n, int k, int* parts_io, unsigned l
     }
     s.adjbits[x] = word;
   }
-  for (int w = threadIdx.x; w < W; w += blockDim.x) s.pmask[w] = 0;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    s.pmask[w] = 0;
+    s.fmask[w] = 0;
+  }
   if (threadIdx.x == 0) *s.flip = 0;
   __syncthreads();
   for (int pass = 0; pass < kMaxPasses; ++pass) {
