@@ -467,8 +467,18 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     const int64_t max_iter = prm.max_iter > 0 ? prm.max_iter : 10ll * nu * m;
     __syncwarp();
 
-    // x = 0, r = b, z = r / diag, p = z  (solver.py:91-97); R and diag in registers
+    // x = 0, r = b, z = r / diag, p = z  (solver.py:91-97); R and diag in registers.
+    // Scalar categorical delta / no vertex kernel (the common case) inline: diag = d d' / kv with
+    // kv in {1, h}; anything else goes through the generic diag_of.
     const bool active = lane < m;
+    const bool vfast = !vlab || (vk.kind == KK_DELTA && ds.nl_dim == 1);
+    double ldeg = 1.0;
+    int llabel = 0;
+    if (vfast && active) {
+      ldeg = ds.deg[L.node_off + lane];
+      if (vlab) llabel = __float_as_int(ds.vlabel[L.node_off + lane]);
+    }
+    const double inv_h = vlab ? 1.0 / (double)fmaxf(vk.h, prm.v_min) : 1.0;
     float rv[NU], dv[NU];
     double rho = 0.0, rr = 0.0;
 #pragma unroll
@@ -478,7 +488,13 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       if (i < nu) {
         float p0 = 0.0f;
         if (active) {
-          dv[i] = (float)diag_of(ds, vk, prm, vlab, U.node_off + i, L.node_off + lane);
+          if (vfast) {
+            const int64_t vu = U.node_off + i;
+            const bool same = !vlab || __float_as_int(ds.vlabel[vu]) == llabel;
+            dv[i] = (float)(ds.deg[vu] * ldeg * (same ? 1.0 : inv_h));
+          } else {
+            dv[i] = (float)diag_of(ds, vk, prm, vlab, U.node_off + i, L.node_off + lane);
+          }
           rv[i] = (float)((double)S.udq[i] * ldq);
           p0 = rv[i] * rcp_approx(dv[i]);
           rho += (double)rv[i] * (double)p0;
