@@ -205,6 +205,41 @@ def _check_gram_vs_oracle(mgk, ds, vspec=("delta", 0.5), espec=("se", 1.0), tol=
             assert abs(int(res.iterations[a, b]) - o.iterations) <= 1, (a, b)
 
 
+def test_edge_case_graphs_vs_oracle(mgk):
+    """Single-node and edgeless graphs, an isolated node beside edges, and the size-class
+    boundaries (24 nodes = largest warp-class graph, 25 = smallest panel-class graph, 33)."""
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(11)
+    iso = mgk.LabeledGraph.from_edges(4, [(0, 1, 1.0), (1, 2, 0.5)], node_labels=np.array([0, 1, 2, 0]),
+                                      edge_labels=np.array([0.25, 1.5]))
+    ds = [mgk.LabeledGraph.from_edges(1, [], node_labels=np.array([2])),
+          mgk.LabeledGraph.from_edges(5, [], node_labels=np.arange(5) % 3), iso,
+          synth.molecule(rng, 2), synth.molecule(rng, 24), synth.molecule(rng, 25), synth.molecule(rng, 33)]
+    _check_gram_vs_oracle(mgk, ds)
+    one = mgk.compute_gram(ds[4:5], "delta:0.5", "se:1.0")
+    o = O.solve_pcg(ds[4], ds[4], ("delta", 0.5), ("se", 1.0))
+    assert one.matrix.shape == (1, 1) and abs(one.matrix[0, 0] - o.value) <= REL * o.value
+    empty = mgk.compute_gram([], "delta:0.5", "se:1.0")
+    assert empty.matrix.shape == (0, 0) and empty.converged.shape == (0, 0)
+    # gram.py:87: a pair that hits max_iterations is NaN and flagged unconverged (no pair here
+    # converges within +-1 iteration of the cap of 8, so the FP32 vectors cannot flip a flag)
+    capped = mgk.compute_gram(ds, "delta:0.5", "se:1.0", mgk.SolverConfig(tolerance=1e-10, max_iterations=8))
+    for a in range(len(ds)):
+        for b in range(a, len(ds)):
+            o = O.solve_pcg(ds[a], ds[b], ("delta", 0.5), ("se", 1.0), tol=1e-10, max_iter=8)
+            assert bool(capped.converged[a, b]) == o.converged, (a, b)
+            if o.converged:
+                assert abs(capped.matrix[a, b] - o.value) <= REL * abs(o.value)
+            else:
+                assert np.isnan(capped.matrix[a, b]) and capped.iterations[a, b] == 8, (a, b)
+    # solver.py:77-121: a single kernel() call reports the best iterate, not NaN
+    cap = mgk.SolverConfig(tolerance=1e-10, max_iterations=8)
+    r = mgk.kernel(ds[4], ds[6], mgk.KroneckerDelta(0.5), mgk.SquareExponential(1.0), cap)
+    o = O.solve_pcg(ds[4], ds[6], ("delta", 0.5), ("se", 1.0), tol=1e-10, max_iter=8)
+    assert not r.converged and r.iterations == 8 and abs(r.value - o.value) <= 1e-4 * abs(o.value)
+
+
 def test_medium_pairs_panel_kernel(mgk):
     # graphs above the warp class (n > 24) go through the CTA-per-pair panel kernel
     # (pcg_panel.cu): self pairs, small x medium (orientation swap), medium x medium
