@@ -413,6 +413,19 @@ def test_pbr_permutations_bit_exact(mgk, golden_structure):
             assert perm.forward.tolist() == rec["pbr"][seed], (rec["name"], seed)
 
 
+def test_pbr_known_answers_on_device(mgk):
+    """Reference tests/test_reorder.py:61-65: two 8-cliques are already optimal (objective 0), and the
+    device permutation equals the oracle's on them and on K24."""
+    cl = [(i, j, 1.0) for i in range(8) for j in range(i + 1, 8)]
+    cl += [(i, j, 1.0) for i in range(8, 16) for j in range(i + 1, 16)]
+    blocks = mgk.LabeledGraph.from_edges(16, cl)
+    k24 = mgk.LabeledGraph.from_edges(24, [(i, j, 1.0) for i in range(24) for j in range(i + 1, 24)])
+    perms = mgk.pbr_reorder_many([blocks, k24], seed=1)
+    assert O.pair_objective(blocks, perms[0].forward // 8) == 0
+    assert perms[0].forward.tolist() == O.pbr_reorder(blocks, 1).tolist()
+    assert perms[1].forward.tolist() == O.pbr_reorder(k24, 1).tolist()
+
+
 def test_pbr_tiles_after_reorder(mgk, golden_structure):
     for rec in golden_structure:
         g = graph_from_json(rec["graph"])

@@ -105,6 +105,38 @@ def test_closed_forms():
     assert O.kernel(p2, p2).value == pytest.approx(0.45, rel=1e-10)
 
 
+def test_operator_known_answers():
+    # reference tests/test_product.py:50-58 (diagonal cache) and :88-94 (apply)
+    from paper_1910_06310_b200.graphs import LabeledGraph
+
+    a = LabeledGraph.from_edges(1, [], node_labels=np.array([0]), stop_prob=[0.3], start_prob=[1.0])
+    b = LabeledGraph.from_edges(1, [], node_labels=np.array([1]), stop_prob=[0.3], start_prob=[1.0])
+    sn = O.ProductSystem(a, b, ("delta", 0.8))
+    assert np.allclose(sn.diag, [0.3 * 0.3 / 0.8], rtol=0, atol=1e-16)
+    assert np.allclose(sn.diag * np.array([2.0]), [0.225])
+    p2 = LabeledGraph.from_edges(2, [(0, 1, 1.0)], stop_prob=[0.5, 0.5])
+    op = O.ProductSystem(p2, p2)
+    assert np.array_equal(op.diag, np.full(4, 2.25))
+    assert np.allclose(op.offdiag(np.ones(4)), np.ones(4), rtol=0, atol=0)
+    assert np.allclose(op.apply(np.ones(4)), np.full(4, 1.25), rtol=1e-15)
+
+
+def test_pbr_known_answers():
+    # reference tests/test_reorder.py:38-65: objective examples, 4-node optimum, block-diagonal 0
+    from paper_1910_06310_b200.graphs import LabeledGraph
+
+    assert O.pair_objective(LabeledGraph.from_edges(6, []), np.arange(6) // 2) == 0
+    four = LabeledGraph.from_edges(4, [(0, 2, 1.0), (1, 3, 1.0)])
+    assert O.pair_objective(four, np.arange(4) // 2) == 1
+    assert O.pair_objective(four, O.pbr_reorder(four, 0, t=2) // 2) == 0
+    k24 = LabeledGraph.from_edges(24, [(i, j, 1.0) for i in range(24) for j in range(i + 1, 24)])
+    assert O.pair_objective(k24, np.arange(24) // 8) == 3
+    cl = [(i, j, 1.0) for i in range(8) for j in range(i + 1, 8)]
+    cl += [(i, j, 1.0) for i in range(8, 16) for j in range(i + 1, 16)]
+    blocks = LabeledGraph.from_edges(16, cl)
+    assert O.pair_objective(blocks, O.pbr_reorder(blocks, 1) // 8) == 0
+
+
 def test_direct_solve_agrees():
     # the oracle's COO product against a dense solve (reference test_solver.py:75-88 triad)
     rng = np.random.default_rng(5)
