@@ -240,6 +240,33 @@ def test_edge_case_graphs_vs_oracle(mgk):
     assert not r.converged and r.iterations == 8 and abs(r.value - o.value) <= 1e-4 * abs(o.value)
 
 
+def _random_graph(mgk, rng, n):
+    """Erdos-Renyi-like graph with random weights, integer node labels and scalar edge labels."""
+    p = min(1.0, rng.uniform(1.5, 4.0 if rng.random() < 0.7 else 12.0) / max(n - 1, 1))
+    ii, jj = np.triu_indices(n, 1)
+    keep = rng.random(ii.size) < p
+    ii, jj = ii[keep], jj[keep]
+    return mgk.LabeledGraph.from_arrays(n, ii, jj, rng.uniform(0.2, 2.0, ii.size),
+                                        node_labels=rng.integers(0, 4, n), edge_labels=rng.uniform(0, 2, ii.size),
+                                        stop_prob=rng.uniform(0.05, 0.5, n))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_random_datasets_vs_oracle(mgk, seed):
+    """Seeded random mixes across every size class (1..200 nodes: tiny, warp, wide, panel), random
+    densities, weights, stopping probabilities and labels; labeled and unlabeled kernels."""
+    rng = np.random.default_rng(100 + seed)
+    sizes = [1, 3] + rng.integers(2, 25, 8).tolist() + rng.integers(25, 121, 4).tolist() + [int(rng.integers(121, 201))]
+    ds = [_random_graph(mgk, rng, int(n)) for n in sizes]
+    # a complete graph on 20 + seed nodes: few nodes but more nonzeros than a warp's slots (380+)
+    k = 20 + seed
+    ii, jj = np.triu_indices(k, 1)
+    ds.append(mgk.LabeledGraph.from_arrays(k, ii, jj, rng.uniform(0.2, 2.0, ii.size), node_labels=rng.integers(0, 4, k),
+                                           edge_labels=rng.uniform(0, 2, ii.size)))
+    _check_gram_vs_oracle(mgk, ds)
+    _check_gram_vs_oracle(mgk, ds[:10] + ds[-1:], None, None, tol=1e-6)  # unlabeled protocol (DESIGN.md)
+
+
 def test_medium_pairs_panel_kernel(mgk):
     # graphs above the warp class (n > 24) go through the CTA-per-pair panel kernel
     # (pcg_panel.cu): self pairs, small x medium (orientation swap), medium x medium
