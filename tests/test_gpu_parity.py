@@ -453,6 +453,17 @@ def test_pbr_known_answers_on_device(mgk):
     assert perms[1].forward.tolist() == O.pbr_reorder(k24, 1).tolist()
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_pbr_random_graphs_bit_exact(mgk, seed):
+    """Device PBR == oracle pbr_reorder on seeded random graphs (9-220 nodes, often disconnected,
+    mixed densities), with the PBR seed varied alongside."""
+    rng = np.random.default_rng(200 + seed)
+    graphs = [_random_graph(mgk, rng, int(n)) for n in rng.integers(9, 221, 8)]
+    perms = mgk.pbr_reorder_many(graphs, seed=seed)
+    for i, (g, perm) in enumerate(zip(graphs, perms)):
+        assert perm.forward.tolist() == O.pbr_reorder(g, seed).tolist(), (i, g.node_count)
+
+
 def test_pbr_tiles_after_reorder(mgk, golden_structure):
     for rec in golden_structure:
         g = graph_from_json(rec["graph"])
