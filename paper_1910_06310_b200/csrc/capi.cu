@@ -767,7 +767,8 @@ static int large_n() {
 // Per-CTA slab (floats) for the block kernel.
 static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl) {
   int64_t el = c->ds.el_dim > 2 ? c->ds.el_dim : 0;
-  int64_t f = 5 * n * m + 8 + 4 * (su + sl) + el * (su + sl) + (n + m + 2) + 16;
+  // + 5 * 128 + 8: a pair with n m <= tiny_nm (<= 128) runs with FP64 vectors (2 floats per element)
+  int64_t f = 5 * n * m + 5 * 128 + 8 + 8 + 4 * (su + sl) + el * (su + sl) + (n + m + 2) + 16;
   return (f + 31) / 32 * 32;
 }
 

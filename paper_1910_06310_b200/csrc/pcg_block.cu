@@ -16,12 +16,13 @@ namespace mgk {
 constexpr int kBlockThreads = 256;
 constexpr int kBlockWarps = kBlockThreads / 32;
 
+template <typename V>
 struct BlockScratch {
-  float* P;
-  float* AP;
-  float* R;
-  float* X;
-  float* DG;
+  V* P;
+  V* AP;
+  V* R;
+  V* X;
+  V* DG;
   float4* UE;   // {col, w, label0, label1}
   float4* LE;
   float* ULAB;  // extra label dims (dim > 2): [S][el_dim]
@@ -110,40 +111,33 @@ __device__ __forceinline__ float block_kappa(const KernelDesc& ek, int kind, con
   return kernel_vec(ek, la, lb, el_dim, cat);
 }
 
-__global__ void __launch_bounds__(kBlockThreads)
-k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
-            unsigned long long* queue, float* scratch, int64_t slab) {
-  __shared__ double red[kBlockWarps];
-  __shared__ unsigned long long sh_pid;
-  __shared__ int sh_carry;
+__device__ __forceinline__ float vfma(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double vfma(double a, double b, double c) { return fma(a, b, c); }
+
+template <typename V>
+__device__ __forceinline__ void solve_block_pair(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,
+                                                 const SolveParams& prm, const SolveOut& out, float* base,
+                                                 unsigned long long pid, int32_t ga, int32_t gb, double* red,
+                                                 int* sh_carry) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int el_dim = ds.el_dim;
   const bool ecat = ds.el_kind == LK_CAT;
   int ekind = prm.labeled ? ek.kind : KK_NONE;
   if (ekind == KK_CONST1) ekind = KK_NONE;
-
-  for (;;) {
-    if (threadIdx.x == 0) sh_pid = atomicAdd(queue, 1ull);
-    __syncthreads();
-    const unsigned long long pid = sh_pid;
-    __syncthreads();
-    if (pid >= (unsigned long long)job.npairs) break;
-    int32_t ga, gb;
-    decode_pair(job, (int64_t)pid, ga, gb);
+  {
     const GraphDesc U = ds.graphs[ga], L = ds.graphs[gb];
     const int n = U.n, m = L.n;
     const int64_t nm = (int64_t)n * m;
     const int SU = 2 * U.ne, SL = 2 * L.ne;
 
-    // carve the slab
-    float* base = scratch + (int64_t)blockIdx.x * slab;
-    BlockScratch s;
-    s.P = base;
+    // carve the slab (block_slab in capi.cu reserves room for FP64 vectors of tiny pairs)
+    BlockScratch<V> s;
+    s.P = reinterpret_cast<V*>((((uintptr_t)base) + 15) & ~(uintptr_t)15);
     s.AP = s.P + nm;
     s.R = s.AP + nm;
     s.X = s.R + nm;
     s.DG = s.X + nm;
-    float* tail = s.DG + nm;
+    float* tail = reinterpret_cast<float*>(s.DG + nm);
     tail = (float*)(((uintptr_t)tail + 15) & ~(uintptr_t)15);
     s.UE = (float4*)tail;
     s.LE = s.UE + SU;
@@ -152,8 +146,8 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     s.urow = (int*)(s.LLAB + (el_dim > 2 ? (int64_t)SL * el_dim : 0));
     s.lrow = s.urow + n + 1;
 
-    block_octiles_to_rows(ds, U, s.UE, s.ULAB, s.urow, &sh_carry);
-    block_octiles_to_rows(ds, L, s.LE, s.LLAB, s.lrow, &sh_carry);
+    block_octiles_to_rows(ds, U, s.UE, s.ULAB, s.urow, sh_carry);
+    block_octiles_to_rows(ds, L, s.LE, s.LLAB, s.lrow, sh_carry);
 
     // diag, b, r, z, p
     const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
@@ -176,12 +170,12 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
       if (vlab)
         kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
                               ds.nl_kind == LK_CAT), prm.v_min);
-      float dg = (float)(ds.deg[vu] * ds.deg[vl]) / kv;
-      float b = (float)((ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]));
-      float z = b / dg;
+      V dg = (V)(ds.deg[vu] * ds.deg[vl]) / (V)kv;
+      V b = (V)((ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]));
+      V z = b / dg;
       s.DG[e] = dg;
       s.R[e] = b;
-      s.X[e] = 0.0f;
+      s.X[e] = V(0);
       s.P[e] = z;
       rho_l += (double)b * z;
       rr_l += (double)b * b;
@@ -199,18 +193,18 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
         const int k0 = s.urow[i], k1 = s.urow[i + 1];
         for (int l = lane; l < m; l += 32) {
           const int q0 = s.lrow[l], q1 = s.lrow[l + 1];
-          float acc = 0.0f;
+          V acc = V(0);
           for (int k = k0; k < k1; ++k) {
             const float4 ea = s.UE[k];
-            const float* prow = s.P + (int64_t)__float_as_int(ea.x) * m;
-            float part = 0.0f;
+            const V* prow = s.P + (int64_t)__float_as_int(ea.x) * m;
+            V part = V(0);
             for (int q = q0; q < q1; ++q) {
               const float4 eb = s.LE[q];
               float kap = block_kappa(ek, ekind, ea, eb, s.ULAB + (int64_t)k * el_dim,
                                       s.LLAB + (int64_t)q * el_dim, el_dim, ecat);
-              part = fmaf(kap * eb.y, prow[__float_as_int(eb.x)], part);
+              part = vfma((V)kap * (V)eb.y, prow[__float_as_int(eb.x)], part);
             }
-            acc = fmaf(ea.y, part, acc);
+            acc = vfma((V)ea.y, part, acc);
           }
           const int64_t e = (int64_t)i * m + l;
           s.AP[e] = s.DG[e] * s.P[e] - acc;
@@ -221,7 +215,7 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
         for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) {
           int i = (int)(e / m), l = (int)(e - (int64_t)i * m);
           if (i < l) {
-            float v = 0.5f * (s.AP[e] + s.AP[(int64_t)l * m + i]);
+            V v = V(0.5) * (s.AP[e] + s.AP[(int64_t)l * m + i]);
             s.AP[e] = v;
             s.AP[(int64_t)l * m + i] = v;
           }
@@ -232,13 +226,13 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
       double pap_l = 0.0;
       for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) pap_l += (double)s.P[e] * (double)s.AP[e];
       const double alpha = rho / block_sum(pap_l, red);
-      const float af = (float)alpha;
+      const V af = (V)alpha;
       double rr2 = 0.0, rz = 0.0;
       for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) {
-        s.X[e] = fmaf(af, s.P[e], s.X[e]);
-        float r = fmaf(-af, s.AP[e], s.R[e]);
+        s.X[e] = vfma(af, s.P[e], s.X[e]);
+        V r = vfma(-af, s.AP[e], s.R[e]);
         s.R[e] = r;
-        float z = r / s.DG[e];
+        V z = r / s.DG[e];
         rr2 += (double)r * r;
         rz += (double)r * z;
       }
@@ -248,8 +242,8 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
         conv = true;
         break;
       }
-      const float beta = (float)(rho_next / rho);
-      for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) s.P[e] = fmaf(beta, s.P[e], s.R[e] / s.DG[e]);
+      const V beta = (V)(rho_next / rho);
+      for (int64_t e = threadIdx.x; e < nm; e += blockDim.x) s.P[e] = vfma(beta, s.P[e], s.R[e] / s.DG[e]);
       rho = rho_next;
       __syncthreads();
     }
@@ -285,6 +279,30 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
         out.K_conv[(int64_t)gb * out.G + ga] = conv;
       }
     }
+  }
+}
+
+__global__ void __launch_bounds__(kBlockThreads)
+k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
+            unsigned long long* queue, float* scratch, int64_t slab) {
+  __shared__ double red[kBlockWarps];
+  __shared__ unsigned long long sh_pid;
+  __shared__ int sh_carry;
+  for (;;) {
+    if (threadIdx.x == 0) sh_pid = atomicAdd(queue, 1ull);
+    __syncthreads();
+    const unsigned long long pid = sh_pid;
+    __syncthreads();
+    if (pid >= (unsigned long long)job.npairs) break;
+    int32_t ga, gb;
+    decode_pair(job, (int64_t)pid, ga, gb);
+    const int64_t nm = (int64_t)ds.graphs[ga].n * ds.graphs[gb].n;
+    // pairs at or below the tiny threshold run with FP64 vectors (CG there ends by Krylov exhaustion,
+    // which FP32 rounding delays; see pcg_warp.cu k_pcg_tiny), the rest with FP32 vectors
+    if (nm <= prm.tiny_nm)
+      solve_block_pair<double>(ds, vk, ek, prm, out, scratch + (int64_t)blockIdx.x * slab, pid, ga, gb, red, &sh_carry);
+    else
+      solve_block_pair<float>(ds, vk, ek, prm, out, scratch + (int64_t)blockIdx.x * slab, pid, ga, gb, red, &sh_carry);
     __syncthreads();
   }
 }

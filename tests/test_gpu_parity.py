@@ -267,6 +267,32 @@ def test_random_datasets_vs_oracle(mgk, seed):
     _check_gram_vs_oracle(mgk, ds[:10] + ds[-1:], None, None, tol=1e-6)  # unlabeled protocol
 
 
+@pytest.mark.parametrize("vs,es,edge_kind", [
+    ("poly:0.5,0.25", "se:0.7", "scalar"),        # polynomial vertex kernel
+    ("delta:0.3", "delta:0.4", "int"),            # categorical-delta edges
+    ("const1", "se:1.5", "vec3"),                 # 3-D vector edge labels (CTA kernel)
+    ("delta:0.5", "prod:se:1.0|delta:0.5", "vec2"),  # composite edge kernel
+])
+def test_random_kernel_families_vs_oracle(mgk, vs, es, edge_kind):
+    """Seeded random graphs (1-60 nodes) under each base-kernel family and edge-label kind."""
+    rng = np.random.default_rng(300)
+    ds = []
+    for n in [1, 2] + rng.integers(3, 61, 8).tolist():
+        g = _random_graph(mgk, rng, int(n))
+        e = g.edge_count
+        lab = {"scalar": rng.uniform(0, 2, e), "int": rng.integers(0, 3, e),
+               "vec3": rng.uniform(0, 1, (e, 3)), "vec2": np.stack([rng.uniform(0, 1, e), rng.integers(0, 2, e)], 1)}
+        ds.append(mgk.LabeledGraph.from_arrays(g.node_count, g.edges_i, g.edges_j, g.weights,
+                                               node_labels=g.node_labels, edge_labels=lab[edge_kind],
+                                               stop_prob=g.stop_prob))
+    res = mgk.compute_gram(ds, vs, es, mgk.SolverConfig(tolerance=1e-10))
+    for a in range(len(ds)):
+        for b in range(a, len(ds)):
+            o = O.solve_pcg(ds[a], ds[b], O.parse_spec(vs), O.parse_spec(es), tol=1e-10)
+            assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value), (a, b, res.matrix[a, b], o.value)
+            assert abs(int(res.iterations[a, b]) - o.iterations) <= 1, (a, b, int(res.iterations[a, b]), o.iterations)
+
+
 def test_medium_pairs_panel_kernel(mgk):
     # graphs above the warp class (n > 24) go through the CTA-per-pair panel kernel
     # (pcg_panel.cu): self pairs, small x medium (orientation swap), medium x medium
