@@ -272,6 +272,9 @@ def test_random_datasets_vs_oracle(mgk, seed):
     ("delta:0.3", "delta:0.4", "int"),            # categorical-delta edges
     ("const1", "se:1.5", "vec3"),                 # 3-D vector edge labels (CTA kernel)
     ("delta:0.5", "prod:se:1.0|delta:0.5", "vec2"),  # composite edge kernel
+    ("se:0.5", "delta:0.4", "int"),               # SE vertex kernel on integer node labels
+    # (RConvolution sums up to dim^2 sub-kernel values, so on random weights the product system is
+    # indefinite; it is covered on the reference's own pairs by test_composite_kernels_golden)
 ])
 def test_random_kernel_families_vs_oracle(mgk, vs, es, edge_kind):
     """Seeded random graphs (1-60 nodes) under each base-kernel family and edge-label kind."""
@@ -291,6 +294,19 @@ def test_random_kernel_families_vs_oracle(mgk, vs, es, edge_kind):
             o = O.solve_pcg(ds[a], ds[b], O.parse_spec(vs), O.parse_spec(es), tol=1e-10)
             assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value), (a, b, res.matrix[a, b], o.value)
             assert abs(int(res.iterations[a, b]) - o.iterations) <= 1, (a, b, int(res.iterations[a, b]), o.iterations)
+
+
+def test_random_pairs_nodewise_pbr_vs_oracle(mgk):
+    """kernel() with PBR reordering on random pairs across the size classes: value, iterations and
+    the un-permuted nodewise field against the oracle on the original node order."""
+    rng = np.random.default_rng(400)
+    for n1, n2 in [(5, 9), (20, 22), (24, 60), (70, 110), (150, 3)]:
+        ga, gb = _random_graph(mgk, rng, n1), _random_graph(mgk, rng, n2)
+        r = mgk.kernel(ga, gb, mgk.KroneckerDelta(0.5), mgk.SquareExponential(1.0), reorder="pbr")
+        o = O.solve_pcg(ga, gb, ("delta", 0.5), ("se", 1.0), tol=1e-10)
+        assert abs(r.value - o.value) <= REL * abs(o.value), (n1, n2)
+        assert abs(r.iterations - o.iterations) <= 1, (n1, n2, r.iterations, o.iterations)
+        assert np.max(np.abs(r.nodewise - o.nodewise)) <= 1e-5 * np.max(np.abs(o.nodewise)), (n1, n2)
 
 
 def test_medium_pairs_panel_kernel(mgk):
