@@ -1333,9 +1333,9 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
     if (a[k] < 0 || a[k] >= c->G || b[k] < 0 || b[k] >= c->G)
       return fail(MGK_E_INVALID, "pair %lld references unknown graph", (long long)k);
   // split into tiny / warp-class / block-class pairs; outputs in job order, remapped below
-  std::vector<int32_t> ta, tb, wa, wb, ba, bb, ga_, gb_;
-  std::vector<int64_t> tidx, widx, bidx, gidx;
-  int64_t bn = 0, bm = 0, bsu = 0, bsl = 0, gn = 0, gm = 0;
+  std::vector<int32_t> ta, tb, wa, wb, ba, bb, ga_, gb_, xa, xb;
+  std::vector<int64_t> tidx, widx, bidx, gidx, xidx;
+  int64_t bn = 0, bm = 0, bsu = 0, bsl = 0, gn = 0, gm = 0, xn = 0, xm = 0, xsu = 0, xsl = 0;
   const bool panel = panel_dataset(c);
   const int T = tiny_nm();
   for (int64_t k = 0; k < npairs; ++k) {
@@ -1345,6 +1345,16 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
       (tiny ? ta : wa).push_back(a[k]);
       (tiny ? tb : wb).push_back(b[k]);
       (tiny ? tidx : widx).push_back(k);
+    } else if (panel && (int64_t)A.n * B.n <= T) {
+      // tiny n m with a graph outside the warp class (a dense small graph): the block solver's FP64
+      // vectors instead of the FP32 panel kernel
+      xa.push_back(a[k]);
+      xb.push_back(b[k]);
+      xidx.push_back(k);
+      xn = std::max<int64_t>(xn, A.n);
+      xm = std::max<int64_t>(xm, B.n);
+      xsu = std::max<int64_t>(xsu, 2 * A.ne);
+      xsl = std::max<int64_t>(xsl, 2 * B.ne);
     } else if (panel && (int64_t)A.n * B.n >= (int64_t)large_n() * large_n()) {
       ga_.push_back(a[k]);
       gb_.push_back(b[k]);
@@ -1368,15 +1378,18 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
   lb.insert(lb.end(), bb.begin(), bb.end());
   la.insert(la.end(), ga_.begin(), ga_.end());
   lb.insert(lb.end(), gb_.begin(), gb_.end());
+  la.insert(la.end(), xa.begin(), xa.end());
+  lb.insert(lb.end(), xb.begin(), xb.end());
   std::vector<int64_t> order(widx);
   order.insert(order.end(), tidx.begin(), tidx.end());
   order.insert(order.end(), bidx.begin(), bidx.end());
   order.insert(order.end(), gidx.begin(), gidx.end());
+  order.insert(order.end(), xidx.begin(), xidx.end());
   cudaStream_t s = c->stream;
   CUDA_TRY(c->d_list_b.upload(la, s));
   CUDA_TRY(c->d_list_c.upload(lb, s));
   const int64_t nw0 = (int64_t)wa.size(), nt0 = (int64_t)ta.size();
-  std::vector<JobSpec> jobs(4);
+  std::vector<JobSpec> jobs(5);
   jobs[0].job = PairJob{PM_LIST, 0, 0, nw0, 0, 1, c->d_list_b.ptr, c->d_list_c.ptr, nullptr, nullptr};
   jobs[0].kernel = JK_WARP;
   jobs[1].job = PairJob{PM_LIST, 0, 0, nt0, 0, 1, c->d_list_b.ptr + nw0, c->d_list_c.ptr + nw0, nullptr, nullptr};
@@ -1394,7 +1407,15 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
   jobs[3].kernel = JK_GRID;
   jobs[3].max_n = gn;
   jobs[3].max_m = gm;
-  std::vector<int64_t> offs = {0, nw0, nw0 + nt0, nw0 + nt0 + nb0};
+  const int64_t nx0 = nw0 + nt0 + nb0 + (int64_t)ga_.size();
+  jobs[4].job = PairJob{PM_LIST, 0, 0, (int64_t)xa.size(), 0, 1, c->d_list_b.ptr + nx0, c->d_list_c.ptr + nx0,
+                        nullptr, nullptr};
+  jobs[4].kernel = JK_BLOCK;
+  jobs[4].max_n = xn;
+  jobs[4].max_m = xm;
+  jobs[4].max_su = xsu;
+  jobs[4].max_sl = xsl;
+  std::vector<int64_t> offs = {0, nw0, nw0 + nt0, nw0 + nt0 + nb0, nx0};
   CUDA_TRY(c->d_value.alloc(npairs));
   CUDA_TRY(c->d_iters.alloc(npairs));
   CUDA_TRY(c->d_conv.alloc(npairs));

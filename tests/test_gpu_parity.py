@@ -309,6 +309,24 @@ def test_random_pairs_nodewise_pbr_vs_oracle(mgk):
         assert np.max(np.abs(r.nodewise - o.nodewise)) <= 1e-5 * np.max(np.abs(o.nodewise)), (n1, n2)
 
 
+def test_dense_small_graph_tiny_pairs(mgk):
+    """A complete K20 (20 nodes, 380 nonzeros: outside the warp class) against a triangle: n m = 60
+    is tiny, so kernel() runs it with FP64 vectors (block solver) and the unlabeled pair matches the
+    oracle's iteration count at the reference default 1e-10, where FP32 vectors stall."""
+    rng = np.random.default_rng(100)
+    sizes = [1, 3] + rng.integers(2, 25, 8).tolist() + rng.integers(25, 121, 4).tolist() + [int(rng.integers(121, 201))]
+    ds = [_random_graph(mgk, rng, int(n)) for n in sizes]
+    ii, jj = np.triu_indices(20, 1)
+    k20 = mgk.LabeledGraph.from_arrays(20, ii, jj, rng.uniform(0.2, 2.0, ii.size), node_labels=rng.integers(0, 4, 20),
+                                       edge_labels=rng.uniform(0, 2, ii.size))
+    for vs, es in [(None, None), ("delta:0.5", "se:1.0")]:
+        for ga, gb in [(ds[1], k20), (k20, ds[1]), (ds[4], k20), (ds[0], k20)]:  # 3, 3, 4, 1 nodes
+            r = mgk.kernel(ga, gb, vs and mgk.KroneckerDelta(0.5), es and mgk.SquareExponential(1.0))
+            o = O.solve_pcg(ga, gb, O.parse_spec(vs), O.parse_spec(es), tol=1e-10)
+            assert abs(r.value - o.value) <= REL * abs(o.value)
+            assert abs(r.iterations - o.iterations) <= 1, (vs, ga.node_count, gb.node_count, r.iterations, o.iterations)
+
+
 def test_medium_pairs_panel_kernel(mgk):
     # graphs above the warp class (n > 24) go through the CTA-per-pair panel kernel
     # (pcg_panel.cu): self pairs, small x medium (orientation swap), medium x medium
