@@ -1042,6 +1042,49 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   return MGK_OK;
 }
 
+// Gram fix-up pass: a graph of at most NU nodes that is outside the warp class (more than SMAX
+// nonzeros, e.g. a complete K20) lands in the mid list, so its pairs with n m <= tiny_nm ran FP32 on the
+// panel kernel.  They are re-solved on the block kernel's FP64 vectors (same canonical a <= b
+// orientation), overwriting the K entries; empty for datasets without such graphs.
+static int gram_fixup_job(mgk_ctx* c, JobSpec& j) {
+  j.job.npairs = 0;
+  if (!panel_dataset(c)) return MGK_OK;  // the block kernel already solved every pair
+  const int T = tiny_nm();
+  std::vector<char> dense(c->G, 0);
+  bool any = false;
+  for (int g = 0; g < c->G; ++g) {
+    const GraphDesc& d = c->graphs[g];
+    dense[g] = d.n <= SmallClass::NU && !small_graph(c, d) && (int64_t)d.n <= T;
+    any = any || dense[g];
+  }
+  if (!any) return MGK_OK;
+  std::vector<int32_t> la, lb;
+  int64_t mn = 0, mm = 0, su = 0, sl = 0;
+  for (int g = 0; g < c->G; ++g) {
+    if (!dense[g]) continue;
+    for (int h = 0; h < c->G; ++h) {
+      if (dense[h] && h < g) continue;  // dense x dense pairs once
+      if ((int64_t)c->graphs[g].n * c->graphs[h].n > T) continue;
+      const int32_t a = std::min(g, h), b = std::max(g, h);
+      la.push_back(a);
+      lb.push_back(b);
+      mn = std::max<int64_t>(mn, c->graphs[a].n);
+      mm = std::max<int64_t>(mm, c->graphs[b].n);
+      su = std::max<int64_t>(su, 2 * c->graphs[a].ne);
+      sl = std::max<int64_t>(sl, 2 * c->graphs[b].ne);
+    }
+  }
+  CUDA_TRY(c->d_list_b.upload(la, c->stream));
+  CUDA_TRY(c->d_list_c.upload(lb, c->stream));
+  j.job = PairJob{PM_LIST, 0, 0, (int64_t)la.size(), 0, 1, c->d_list_b.ptr, c->d_list_c.ptr, nullptr, nullptr};
+  j.kernel = JK_BLOCK;
+  j.max_n = mn;
+  j.max_m = mm;
+  j.max_su = su;
+  j.max_sl = sl;
+  return MGK_OK;
+}
+
 int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv) {
   if (!c) return fail(MGK_E_INVALID, "null context");
   if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
@@ -1062,6 +1105,16 @@ int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters
   std::vector<int64_t> offs(jobs.size(), 0);
   rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
   if (rc) return rc;
+  std::vector<JobSpec> fix(1);
+  rc = gram_fixup_job(c, fix[0]);
+  if (rc) return rc;
+  if (fix[0].job.npairs > 0) {
+    const double ms = c->last_ms;
+    std::vector<int64_t> off1(1, 0);
+    rc = run_jobs(c, fix, o, off1, make_params(c, tol, max_iter));
+    if (rc) return rc;
+    c->last_ms += ms;
+  }
   if (K) CUDA_TRY(d2h(K, c->d_K.ptr, G * G * sizeof(double)));
   if (iters) CUDA_TRY(d2h(iters, c->d_Kit.ptr, G * G * sizeof(int32_t)));
   if (conv) CUDA_TRY(d2h(conv, c->d_Kconv.ptr, G * G));

@@ -311,8 +311,8 @@ def test_random_pairs_nodewise_pbr_vs_oracle(mgk):
 
 def test_dense_small_graph_tiny_pairs(mgk):
     """A complete K20 (20 nodes, 380 nonzeros: outside the warp class) against a triangle: n m = 60
-    is tiny, so kernel() runs it with FP64 vectors (block solver) and the unlabeled pair matches the
-    oracle's iteration count at the reference default 1e-10, where FP32 vectors stall."""
+    is tiny, so kernel() and the Gram run it with FP64 vectors (block solver) and the unlabeled pair
+    matches the oracle's iteration count at the reference default 1e-10, where FP32 vectors stall."""
     rng = np.random.default_rng(100)
     sizes = [1, 3] + rng.integers(2, 25, 8).tolist() + rng.integers(25, 121, 4).tolist() + [int(rng.integers(121, 201))]
     ds = [_random_graph(mgk, rng, int(n)) for n in sizes]
@@ -325,6 +325,18 @@ def test_dense_small_graph_tiny_pairs(mgk):
             o = O.solve_pcg(ga, gb, O.parse_spec(vs), O.parse_spec(es), tol=1e-10)
             assert abs(r.value - o.value) <= REL * abs(o.value)
             assert abs(r.iterations - o.iterations) <= 1, (vs, ga.node_count, gb.node_count, r.iterations, o.iterations)
+    # the Gram re-solves the same pairs on the FP64 block path (gram_fixup_job, capi.cu); K20 x K20
+    # (n m = 400) is not tiny and keeps the unlabeled FP32 protocol, so it is left out here
+    gs = [ds[0], ds[1], ds[4], k20]
+    res = mgk.compute_gram(gs, None, None, mgk.SolverConfig(tolerance=1e-10))
+    for a in range(4):
+        for b in range(a, 4):
+            if gs[a].node_count * gs[b].node_count > 128:
+                continue
+            o = O.solve_pcg(gs[a], gs[b], None, None, tol=1e-10)
+            assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value), (a, b)
+            assert abs(int(res.iterations[a, b]) - o.iterations) <= 1, (a, b, int(res.iterations[a, b]), o.iterations)
+    _check_gram_vs_oracle(mgk, [ds[0], ds[1], ds[4], k20, ds[2]])
 
 
 def test_medium_pairs_panel_kernel(mgk):
