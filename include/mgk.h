@@ -64,6 +64,13 @@ int mgk_upload(mgk_ctx* ctx, int32_t N, const int64_t* node_off, const int64_t* 
  * similarity, product.py:172; edge: kappa = 1, product.py:74-79). */
 int mgk_set_kernels(mgk_ctx* ctx, const char* vertex_spec, const char* edge_spec);
 
+/* Vertex-similarity floor v_min of the solves that follow (SolverConfig.v_min,
+ * solver.py:39-52, threaded into vertex_similarity_matrix by solver.py:241-242,
+ * product.py:164-178): kv = max(kappa_v, v_min); a floored similarity <= 0
+ * fails the solve with MGK_E_INVALID "vertex kernel produced non-positive
+ * similarity".  Default 1e-12 (DEFAULT_VERTEX_FLOOR). */
+int mgk_set_vertex_floor(mgk_ctx* ctx, double v_min);
+
 /* Per-graph partition-based reordering on the device (pbr_reorder,
  * reorder.py:361-404), same seed for every graph (solver.py:236-237).
  * Writes forward maps (old -> new) into perms_out[sum n] when non-NULL.  With

@@ -288,6 +288,9 @@ struct mgk_ctx {
   DBuf<GraphDesc> d_graphs;
   DBuf<float> d_p, d_q, d_vlabel, d_ew, d_elabel, d_nzw, d_nzlabel;
   DBuf<double> d_q64, d_deg;
+  DBuf<float> d_dm;
+  DBuf<int32_t> d_status;
+  double v_min = 1e-12;  // SolverConfig.v_min (solver.py:39-52), mgk_set_vertex_floor
   DBuf<int32_t> d_ei, d_ej, d_egraph, d_ngraph, d_trow, d_segcount, d_segcursor, d_segntiles, d_seggraph, d_segrow;
   DBuf<int64_t> d_gseg, d_segstart, d_segtile;
   DBuf<uint64_t> d_keys, d_keys2;
@@ -467,6 +470,13 @@ int mgk_upload(mgk_ctx* c, int32_t N, const int64_t* node_off, const int64_t* ed
   return MGK_OK;
 }
 
+int mgk_set_vertex_floor(mgk_ctx* c, double v_min) {
+  if (!c) return fail(MGK_E_INVALID, "null context");
+  if (std::isnan(v_min)) return fail(MGK_E_INVALID, "v_min must be a number");
+  c->v_min = v_min;
+  return MGK_OK;
+}
+
 int mgk_set_kernels(mgk_ctx* c, const char* vertex_spec, const char* edge_spec) {
   if (!c) return fail(MGK_E_INVALID, "null context");
   Spec vs, es;
@@ -551,8 +561,10 @@ static int build_octiles(mgk_ctx* c) {
   }
   k_trow<<<(G + 127) / 128, 128, 0, s>>>(G, c->d_gseg.ptr, c->d_segtile.ptr, c->d_graphs.ptr, c->d_trow.ptr);
   CUDA_TRY(c->d_deg.alloc(nn));
+  CUDA_TRY(c->d_dm.alloc(nn));
   k_degrees<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(nn, c->d_ngraph.ptr, c->d_graphs.ptr, c->d_tiles.ptr,
-                                                         c->d_trow.ptr, c->d_nzw.ptr, c->d_q64.ptr, c->d_deg.ptr);
+                                                         c->d_trow.ptr, c->d_nzw.ptr, c->d_q64.ptr, c->d_deg.ptr,
+                                                         c->d_dm.ptr);
   CUDA_TRY(cudaGetLastError());
   c->graphs.resize(G);
   CUDA_TRY(cudaMemcpyAsync(c->graphs.data(), c->d_graphs.ptr, G * sizeof(GraphDesc), cudaMemcpyDeviceToHost, s));
@@ -562,6 +574,8 @@ static int build_octiles(mgk_ctx* c) {
   c->ds.nz_w = c->d_nzw.ptr;
   c->ds.nz_label = c->d_nzlabel.ptr;
   c->ds.deg = c->d_deg.ptr;
+  c->ds.dm = c->d_dm.ptr;
+  c->ds.q64 = c->d_q64.ptr;
   return MGK_OK;
 }
 
@@ -619,6 +633,16 @@ static int prepare(mgk_ctx* c) {
       d.npanels = (int32_t)(panels.size() - d.panel_off - 1);
     } else {
       d.npanels = 0;
+    }
+    {  // max d_i / q_i (host FP64; only steers the Laplacian-splitting switch)
+      std::vector<double> dd(d.n, 0.0);
+      for (int64_t e = c->edge_off[g]; e < c->edge_off[g + 1]; ++e) {
+        dd[c->ei[e]] += c->w[e];
+        dd[c->ej[e]] += c->w[e];
+      }
+      double r = 1.0;
+      for (int i = 0; i < d.n; ++i) r = std::max(r, (dd[i] + c->q[c->node_off[g] + i]) / c->q[c->node_off[g] + i]);
+      d.dqr = (float)std::min(r, 3.0e38);
     }
     gd[g] = d;
     for (int64_t i = c->node_off[g]; i < c->node_off[g + 1]; ++i) ngraph[i] = g;
@@ -724,12 +748,21 @@ static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   SolveParams p{};
   p.tol2 = tol * tol;
   p.max_iter = max_iter;
-  p.v_min = 1e-12f;
+  p.v_min = (float)c->v_min;
   p.tiny_nm = tiny_nm();
+  p.lap_mode = getenv("MGK_LAPLACIAN") ? std::max(0, std::min(2, atoi(getenv("MGK_LAPLACIAN")))) : 1;
   p.panel_rpc = getenv("MGK_PANEL_RPC") ? atoi(getenv("MGK_PANEL_RPC")) : 0;
   // product.py:153-161 with dataset-uniform label presence; kappa = 1 when ek is None/const1
   p.labeled = (c->el_kind != LK_NONE && c->espec.kind != KK_NONE && c->espec.kind != KK_CONST1) ? 1 : 0;
   return p;
+}
+
+// Solver status bits -> the reference's errors (vertex_similarity_matrix, product.py:176-177).
+static int check_status(mgk_ctx* c) {
+  int32_t st = 0;
+  CUDA_TRY(cudaMemcpy(&st, c->d_status.ptr, sizeof st, cudaMemcpyDeviceToHost));
+  if (st & kStatusNonPositiveKv) return fail(MGK_E_INVALID, "vertex kernel produced non-positive similarity");
+  return MGK_OK;
 }
 
 enum JobKernel { JK_BLOCK = 0, JK_WARP = 1, JK_TINY = 2, JK_PANEL = 3, JK_GRID = 4 };
@@ -767,8 +800,9 @@ static int large_n() {
 // Per-CTA slab (floats) for the block kernel.
 static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl) {
   int64_t el = c->ds.el_dim > 2 ? c->ds.el_dim : 0;
-  // + 5 * 128 + 8: a pair with n m <= tiny_nm (<= 128) runs with FP64 vectors (2 floats per element)
-  int64_t f = 5 * n * m + 5 * 128 + 8 + 8 + 4 * (su + sl) + el * (su + sl) + (n + m + 2) + 16;
+  // 6 vectors (P, AP, R, X, DG, SD); + 6 * 128 + 8: a pair with n m <= tiny_nm (<= 128) runs with FP64
+  // vectors (2 floats per element)
+  int64_t f = 6 * n * m + 6 * 128 + 8 + 8 + 4 * (su + sl) + el * (su + sl) + (n + m + 2) + 16;
   return (f + 31) / 32 * 32;
 }
 
@@ -798,7 +832,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
       ctas[k] = 2 * c->num_sms;
     } else if (j.kernel == JK_PANEL) {
       const int64_t nm = j.max_n * j.max_m;
-      slabs[k] = 6 * ((nm + 31) / 32 * 32);
+      slabs[k] = kSlabVectors * ((nm + 31) / 32 * 32);
       // P and Ap in shared memory when every pair of the job fits; else all pairs keep them in HBM/L2
       // and the whole L1 stays available to the gathers
       const int64_t smem_nm = getenv("MGK_PANEL_SMEM_NM") ? atoll(getenv("MGK_PANEL_SMEM_NM")) : kPanelSmemNM;
@@ -823,10 +857,13 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   for (auto& j : jobs)
     if (j.kernel == JK_GRID && j.job.npairs > 0) grid_vstride = std::max(grid_vstride, (j.max_n * j.max_m + 31) / 32 * 32);
   if (grid_vstride > 0) {
-    CUDA_TRY(c->d_gridvec.alloc((size_t)(6 * grid_vstride)));
+    CUDA_TRY(c->d_gridvec.alloc((size_t)(kSlabVectors * grid_vstride)));
     CUDA_TRY(c->d_gridbuf.alloc((size_t)(2 * gblocks)));
   }
   c->last_launches = 0;
+  CUDA_TRY(c->d_status.alloc(1));
+  // asynchronous callers (the nodewise stream) clear the status once and check it at the end
+  if (sync) CUDA_TRY(cudaMemsetAsync(c->d_status.ptr, 0, sizeof(int32_t), s));
   CUDA_TRY(cudaEventRecord(e0, s));
   // Streams: grid and CTA-class jobs in order on the main stream (they share the scratch slabs and the
   // cooperative grid must own the device); warp-class jobs on side stream 0, tiny jobs on side stream
@@ -849,6 +886,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     JobSpec& j = jobs[k];
     if (j.job.npairs <= 0) continue;
     SolveOut o = out_base;
+    o.status = c->d_status.ptr;
     int64_t off = out_offsets[k];
     if (o.value) o.value += off;
     if (o.iters) o.iters += off;
@@ -891,7 +929,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
   float ms = 0.0f;
   cudaEventElapsedTime(&ms, e0, e1);
   c->last_ms = ms;
-  return MGK_OK;
+  return check_status(c);
 }
 
 // Gram jobs (all pairs a <= b, gram.py:57-95), cost-descending within each:
@@ -1272,6 +1310,8 @@ int mgk_gram_nodewise(mgk_ctx* c, int rank, int world, double tol, int64_t max_i
       cudaEventDestroy(slot[k].done);
     }
   };
+  CUDA_TRY(c->d_status.alloc(1));
+  CUDA_TRY(cudaMemsetAsync(c->d_status.ptr, 0, sizeof(int32_t), c->stream));
   int64_t total_pairs = 0, total_floats = 0;
   double ms_total = 0.0;
   int launches = 0, pending = -1, chunk = 0;
@@ -1367,6 +1407,8 @@ int mgk_gram_nodewise(mgk_ctx* c, int rank, int world, double tol, int64_t max_i
     }
   }
   destroy();
+  rc = check_status(c);
+  if (rc) return rc;
   c->last_ms = ms_total;
   c->last_launches = launches;
   if (npairs_out) *npairs_out = total_pairs;

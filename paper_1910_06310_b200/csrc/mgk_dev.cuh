@@ -50,8 +50,18 @@ struct GraphDesc {
   int64_t rowptr_off; // into the row-pointer array (n + 1 entries, = node_off + graph index)
   int64_t panel_off;  // into the panel row-boundary array (npanels + 1 entries)
   int32_t npanels;    // row panels of <= kPanelCap nonzeros (0 if a row exceeds the cap)
-  int32_t pad;
+  float dqr;          // max_i d_i / q_i: drives the Laplacian-splitting switch (laplacian_pair)
 };
+
+// SURVEY.md §7 H1.  For kappa_e = 1 the operator's diagonal d d'/kv and the row
+// sums of the off-diagonal part (d - q)(d' - q') nearly cancel when q << d, so
+// FP32 diag * p - XMV(p) loses log10(diag / s) digits, s = diag - rowsum.  With
+// the Laplacian splitting the solvers form
+//   A p = s * p - sum_{jj'} L_{ii',jj'} (p_jj' - p_ii'),   s in FP64,
+// whose FP32 terms are differences of nearby values.  The cancellation factor
+// diag / s ~ a b / (a + b) with a, b the graphs' max d/q; pairs above
+// kLapFactor (error ~3e-8 x factor without the splitting) switch it on.
+constexpr float kLapFactor = 32.0f;
 
 // Row panels (pcg_panel.cu): consecutive rows whose nonzeros fit 32 lanes x kPanelSlots.
 #ifndef MGK_PANEL_SLOTS
@@ -136,6 +146,8 @@ struct DatasetDev {
   const float* p;
   const float* q;
   const double* deg;           // d_i = sum_j w_ij + q_i, accumulated in ascending column order (f64)
+  const double* q64;           // q_i (f64)
+  const float* dm;             // d_i - q_i (= the FP32 row sum of the weights), Laplacian splitting
   const float* vlabel;         // [sum n * nl_dim]  (categorical tokens stored as int bits)
   // octiles
   const Octile* tiles;

@@ -42,7 +42,10 @@ struct SolveOut {
   // nodewise field x[i * m + i'] per pair (float32), offsets per pair id
   float* nodewise;
   const int64_t* nodewise_off;
+  // status bits raised by the solvers (kStatusNonPositiveKv: a floored vertex similarity <= 0)
+  int32_t* status;
 };
+constexpr int32_t kStatusNonPositiveKv = 1;
 
 struct SolveParams {
   double tol2;              // tol^2 (relative stopping rule r.r < tol^2 b.b)
@@ -51,7 +54,22 @@ struct SolveParams {
   int32_t labeled;          // edge mode decided per dataset (product.py:153-161)
   int32_t tiny_nm;          // n*m at or below which the warp solver runs the pair in FP64
   int32_t panel_rpc;        // U rows per panel work item (0: automatic)
+  int32_t lap_mode;         // Laplacian splitting (kappa_e = 1 pairs): 0 off, 1 by factor, 2 always
 };
+
+// Laplacian splitting for this pair (mgk_dev.cuh kLapFactor); only the kappa_e = 1 solvers read it.
+__host__ __device__ inline bool laplacian_pair(const SolveParams& prm, const GraphDesc& a, const GraphDesc& b) {
+  if (prm.lap_mode <= 0) return false;
+  if (prm.lap_mode >= 2) return true;
+  return a.dqr * b.dqr > kLapFactor * (a.dqr + b.dqr);
+}
+
+// kv = max(kappa_v, v_min) with the reference's non-positive check (product.py:164-178)
+__device__ __forceinline__ float floor_kv(float kv, const SolveParams& prm, const SolveOut& out) {
+  kv = fmaxf(kv, prm.v_min);
+  if (!(kv > 0.0f) && out.status) atomicOr(out.status, kStatusNonPositiveKv);
+  return kv;
+}
 
 // Gram modes report a <= b (the reference's pair order, gram.py:38-54); lists keep the caller's order.
 __host__ __device__ inline void decode_gram_pair(const PairJob& j, int64_t pid, int32_t& a, int32_t& b);
@@ -109,12 +127,15 @@ __global__ void k_seg_emit(int64_t, const int64_t*, const int32_t*, const int64_
                            const int32_t*, const uint64_t*, const GraphDesc*, const float*, const float*, int,
                            Octile*, float*, float*);
 __global__ void k_degrees(int64_t, const int32_t*, const GraphDesc*, const Octile*, const int32_t*,
-                          const float*, const double*, double*);
+                          const float*, const double*, double*, float*);
 __global__ void k_scan_exclusive(int64_t, const int32_t*, int64_t*);
 __global__ void k_trow(int, const int64_t*, const int64_t*, GraphDesc*, int32_t*);
 __global__ void k_rows_fill(int64_t, const int32_t*, const GraphDesc*, const Octile*, const int32_t*, const float*,
                             const float*, int, const int32_t*, float4*);
 constexpr int kSortSmemBytes = 8192 * 8;
+
+// per-pair FP32 vectors of the panel slab / grid buffer (pcg_panel.cu)
+constexpr int kSlabVectors = 7;
 
 // ---- solvers (pcg_warp.cu, pcg_block.cu)
 struct SmallClass {

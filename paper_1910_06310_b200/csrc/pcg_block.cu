@@ -23,6 +23,7 @@ struct BlockScratch {
   V* R;
   V* X;
   V* DG;
+  V* SD;        // Laplacian splitting: s = diag - rowsum(L)
   float4* UE;   // {col, w, label0, label1}
   float4* LE;
   float* ULAB;  // extra label dims (dim > 2): [S][el_dim]
@@ -137,7 +138,8 @@ __device__ __forceinline__ void solve_block_pair(const DatasetDev& ds, const Ker
     s.R = s.AP + nm;
     s.X = s.R + nm;
     s.DG = s.X + nm;
-    float* tail = reinterpret_cast<float*>(s.DG + nm);
+    s.SD = s.DG + nm;
+    float* tail = reinterpret_cast<float*>(s.SD + nm);
     tail = (float*)(((uintptr_t)tail + 15) & ~(uintptr_t)15);
     s.UE = (float4*)tail;
     s.LE = s.UE + SU;
@@ -149,15 +151,17 @@ __device__ __forceinline__ void solve_block_pair(const DatasetDev& ds, const Ker
     block_octiles_to_rows(ds, U, s.UE, s.ULAB, s.urow, sh_carry);
     block_octiles_to_rows(ds, L, s.LE, s.LLAB, s.lrow, sh_carry);
 
+    // kappa_e = 1 pairs with a large diag / s (mgk_dev.cuh kLapFactor): A p = s p - sum L (p_j - p_i)
+    const bool lap = ekind == KK_NONE && laplacian_pair(prm, U, L);
     // diag, b, r, z, p
     const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
     double bu = 0.0, bl = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      double dq = ds.deg[U.node_off + i] * (double)ds.q[U.node_off + i];
+      double dq = ds.deg[U.node_off + i] * ds.q64[U.node_off + i];
       bu += dq * dq;
     }
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      double dq = ds.deg[L.node_off + i] * (double)ds.q[L.node_off + i];
+      double dq = ds.deg[L.node_off + i] * ds.q64[L.node_off + i];
       bl += dq * dq;
     }
     const double bb = block_sum(bu, red) * block_sum(bl, red);
@@ -168,10 +172,12 @@ __device__ __forceinline__ void solve_block_pair(const DatasetDev& ds, const Ker
       int64_t vu = U.node_off + i, vl = L.node_off + l;
       float kv = 1.0f;
       if (vlab)
-        kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
-                              ds.nl_kind == LK_CAT), prm.v_min);
-      V dg = (V)(ds.deg[vu] * ds.deg[vl]) / (V)kv;
-      V b = (V)((ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]));
+        kv = floor_kv(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
+                                 ds.nl_kind == LK_CAT), prm, out);
+      const double dg64 = ds.deg[vu] * ds.deg[vl] / (double)kv;
+      V dg = (V)dg64;
+      s.SD[e] = lap ? (V)(dg64 - (ds.deg[vu] - ds.q64[vu]) * (ds.deg[vl] - ds.q64[vl])) : dg;
+      V b = (V)((ds.deg[vu] * ds.q64[vu]) * (ds.deg[vl] * ds.q64[vl]));
       V z = b / dg;
       s.DG[e] = dg;
       s.R[e] = b;
@@ -193,6 +199,8 @@ __device__ __forceinline__ void solve_block_pair(const DatasetDev& ds, const Ker
         const int k0 = s.urow[i], k1 = s.urow[i + 1];
         for (int l = lane; l < m; l += 32) {
           const int q0 = s.lrow[l], q1 = s.lrow[l + 1];
+          const int64_t e = (int64_t)i * m + l;
+          const V pc = lap ? s.P[e] : V(0);
           V acc = V(0);
           for (int k = k0; k < k1; ++k) {
             const float4 ea = s.UE[k];
@@ -202,12 +210,11 @@ __device__ __forceinline__ void solve_block_pair(const DatasetDev& ds, const Ker
               const float4 eb = s.LE[q];
               float kap = block_kappa(ek, ekind, ea, eb, s.ULAB + (int64_t)k * el_dim,
                                       s.LLAB + (int64_t)q * el_dim, el_dim, ecat);
-              part = vfma((V)kap * (V)eb.y, prow[__float_as_int(eb.x)], part);
+              part = vfma((V)kap * (V)eb.y, prow[__float_as_int(eb.x)] - pc, part);
             }
             acc = vfma((V)ea.y, part, acc);
           }
-          const int64_t e = (int64_t)i * m + l;
-          s.AP[e] = s.DG[e] * s.P[e] - acc;
+          s.AP[e] = s.SD[e] * s.P[e] - acc;
         }
       }
       __syncthreads();

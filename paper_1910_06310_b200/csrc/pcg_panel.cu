@@ -51,6 +51,9 @@ constexpr int kCacheU = 1024;
 constexpr int kCacheRows = 256;
 constexpr int kCacheFloats = 4 * (kCacheU + kPanelCap) + 2 * (kCacheRows + 1) + 2;
 constexpr int kPanelStaticSmem = (kPW * kSegFloats + kCacheFloats) * 4;
+// Per-pair vectors in the panel slab / grid buffer: R, DG, X, P, AP, T (unlabeled: P B^T), SD (the
+// shifted diagonal s of the Laplacian splitting).  capi.cu sizes both with kSlabVectors (mgk_internal.h).
+static_assert(kSlabVectors == 7, "slab layout");
 
 __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -71,10 +74,13 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
 }
 
 // acc[t] += sum_{k in [k0, k1)} kappa(e_k, e'_t) w_k P[j_k][lcol[t]]   (U row, warp-uniform)
-template <int NS, int EK>
+// LAP (kappa_e = 1, Laplacian splitting): the gathered values enter as differences P[j_k][lcol[t]] - pc[t]
+// with pc[t] = P[i][row(t)] the element the contribution lands on (mgk_dev.cuh kLapFactor).
+template <int NS, int EK, bool LAP = false>
 __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float4* __restrict__ ue, int k0, int k1,
                                                const float* P, int m, const int (&lcol)[NS],
-                                               const float (&llab)[NS], float (&acc)[NS]) {
+                                               const float (&llab)[NS], float (&acc)[NS],
+                                               const float (&pc)[NS]) {
   int k = k0;
   for (; k + 1 < k1; k += 2) {
     const float4 e0 = ue[k], e1 = ue[k + 1];
@@ -85,6 +91,10 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
     for (int t = 0; t < NS; ++t) {
       p0[t] = r0[lcol[t]];
       p1[t] = r1[lcol[t]];
+      if constexpr (LAP) {
+        p0[t] -= pc[t];
+        p1[t] -= pc[t];
+      }
     }
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
@@ -97,7 +107,28 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
     const float* r0 = P + __float_as_int(e0.x) * m;
 #pragma unroll
     for (int t = 0; t < NS; ++t)
-      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y), r0[lcol[t]], acc[t]);
+      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y),
+                    LAP ? r0[lcol[t]] - pc[t] : r0[lcol[t]], acc[t]);
+  }
+}
+
+// L row of every slot of a panel (Laplacian splitting): lrow[t] = r with lrp[r] <= kbeg + lane + 32 t < lrp[r+1]
+template <int NS>
+__device__ __forceinline__ void slot_rows(const int32_t* lrp, int rbeg, int rend, int kbeg, int kend, int lane,
+                                          int (&lrow)[NS]) {
+#pragma unroll
+  for (int t = 0; t < NS; ++t) {
+    const int k = kbeg + lane + 32 * t;
+    int lo = rbeg, hi = rend;  // largest r in [rbeg, rend) with lrp[r] <= k
+    if (k >= kend) {
+      lrow[t] = rbeg;
+      continue;
+    }
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (lrp[mid] <= k) lo = mid; else hi = mid;
+    }
+    lrow[t] = lo;
   }
 }
 
@@ -114,7 +145,8 @@ struct PairView {
 // AP = diag * P - XMV(P) over the (panel, chunk) items w0, w0 + wstride, ...
 // When part != nullptr the warp also accumulates (p.Ap, px.p) over the
 // elements it wrote (every element is written by exactly one item).
-template <int NS, int EK>
+// LAP: AP = s * P - sum L (P_jj' - P_ii') with DG = s (the caller passes the shifted diagonal).
+template <int NS, int EK, bool LAP = false>
 __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float* P, float* AP, const float* DG,
                            float* SEG, int lane, int64_t w0, int64_t wstride, const float* pu, const float* pl,
                            double2* part) {
@@ -142,6 +174,8 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
         llab[t] = e.z;
       }
     }
+    int lrw[NS];
+    if constexpr (LAP) slot_rows<NS>(v.lrp, rbeg, rend, kbeg, kend, lane, lrw);
     // this lane's first two panel rows, cached
     const int ra = rbeg + lane, rb = rbeg + lane + 32;
     int qa0 = 0, qa1 = 0, qb0 = 0, qb1 = 0;
@@ -159,11 +193,18 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
     const int i0 = c * v.rpc, i1 = min(n, i0 + v.rpc);
     for (int i = i0; i < i1; i += 2) {
       const bool two = i + 1 < i1;
-      float acc0[NS], acc1[NS];
+      float acc0[NS], acc1[NS], pc0[NS], pc1[NS];
 #pragma unroll
-      for (int t = 0; t < NS; ++t) acc0[t] = acc1[t] = 0.0f;
-      row_accumulate<NS, EK>(ek, v.ue, v.urp[i], v.urp[i + 1], P, m, lcol, llab, acc0);
-      if (two) row_accumulate<NS, EK>(ek, v.ue, v.urp[i + 1], v.urp[i + 2], P, m, lcol, llab, acc1);
+      for (int t = 0; t < NS; ++t) {
+        acc0[t] = acc1[t] = 0.0f;
+        pc0[t] = pc1[t] = 0.0f;
+        if constexpr (LAP) {
+          pc0[t] = P[i * m + lrw[t]];
+          if (two) pc1[t] = P[(i + 1) * m + lrw[t]];
+        }
+      }
+      row_accumulate<NS, EK, LAP>(ek, v.ue, v.urp[i], v.urp[i + 1], P, m, lcol, llab, acc0, pc0);
+      if (two) row_accumulate<NS, EK, LAP>(ek, v.ue, v.urp[i + 1], v.urp[i + 2], P, m, lcol, llab, acc1, pc1);
 #pragma unroll
       for (int t = 0; t < NS; ++t) {
         SEG[lane + 32 * t] = acc0[t] * lw[t];
@@ -227,7 +268,18 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
 template <int EK>
 __device__ __forceinline__ void xmv_dispatch(int ns, const KernelDesc& ek, const PairView& v, const float* P,
                                              float* AP, const float* DG, float* SEG, int lane, int64_t w0,
-                                             int64_t wstride, const float* pu, const float* pl, double2* part) {
+                                             int64_t wstride, const float* pu, const float* pl, double2* part,
+                                             bool lap) {
+  if constexpr (EK == KK_NONE) {
+    if (lap) {
+      switch (ns) {
+        case 2: xmv_panels<2, EK, true>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
+        case 4: xmv_panels<4, EK, true>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
+        default: xmv_panels<kPanelSlots, EK, true>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
+      }
+      return;
+    }
+  }
   switch (ns) {
     case 2: xmv_panels<2, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
     case 4: xmv_panels<4, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part); break;
@@ -242,7 +294,8 @@ __device__ __forceinline__ void xmv_dispatch(int ns, const KernelDesc& ek, const
 //             the panel's slots in registers, segment sums as in xmv_panels)
 //   phase AP: AP[i][r] = diag P - sum_{k in U(i)} w_k T[j_k][r]  (thread per element, coalesced over r)
 // The caller places a block / grid barrier between the phases.
-template <int NS>
+// LAP: T[j][r] = sum_{t in L(r)} w'_t (P[j][col(t)] - P[j][r])  (Laplacian splitting, see factored_AP)
+template <int NS, bool LAP>
 __device__ void factored_T(const PairView& v, const float* P, float* T, float* SEG, int lane, int64_t w0,
                            int64_t wstride) {
   const int n = v.n, m = v.m;
@@ -266,6 +319,8 @@ __device__ void factored_T(const PairView& v, const float* P, float* T, float* S
         lw[t] = e.y;
       }
     }
+    int lrw[NS];
+    if constexpr (LAP) slot_rows<NS>(v.lrp, rbeg, rend, kbeg, kend, lane, lrw);
     const int j0 = c * v.rpc, j1 = min(n, j0 + v.rpc);
     for (int j = j0; j < j1; j += 2) {
       const bool two = j + 1 < j1;
@@ -273,8 +328,13 @@ __device__ void factored_T(const PairView& v, const float* P, float* T, float* S
       const float* r1 = two ? r0 + m : r0;
 #pragma unroll
       for (int t = 0; t < NS; ++t) {
-        SEG[lane + 32 * t] = lw[t] * r0[lcol[t]];
-        SEG[kPanelCap + lane + 32 * t] = lw[t] * r1[lcol[t]];
+        float x0 = r0[lcol[t]], x1 = r1[lcol[t]];
+        if constexpr (LAP) {
+          x0 -= r0[lrw[t]];
+          x1 -= r1[lrw[t]];
+        }
+        SEG[lane + 32 * t] = lw[t] * x0;
+        SEG[kPanelCap + lane + 32 * t] = lw[t] * x1;
       }
       __syncwarp();
       for (int r = rbeg + lane; r < rend; r += 32) {
@@ -293,17 +353,28 @@ __device__ void factored_T(const PairView& v, const float* P, float* T, float* S
 }
 
 __device__ __forceinline__ void factored_T_dispatch(int ns, const PairView& v, const float* P, float* T, float* SEG,
-                                                    int lane, int64_t w0, int64_t wstride) {
+                                                    int lane, int64_t w0, int64_t wstride, bool lap) {
+  if (lap) {
+    switch (ns) {
+      case 2: factored_T<2, true>(v, P, T, SEG, lane, w0, wstride); break;
+      case 4: factored_T<4, true>(v, P, T, SEG, lane, w0, wstride); break;
+      default: factored_T<kPanelSlots, true>(v, P, T, SEG, lane, w0, wstride); break;
+    }
+    return;
+  }
   switch (ns) {
-    case 2: factored_T<2>(v, P, T, SEG, lane, w0, wstride); break;
-    case 4: factored_T<4>(v, P, T, SEG, lane, w0, wstride); break;
-    default: factored_T<kPanelSlots>(v, P, T, SEG, lane, w0, wstride); break;
+    case 2: factored_T<2, false>(v, P, T, SEG, lane, w0, wstride); break;
+    case 4: factored_T<4, false>(v, P, T, SEG, lane, w0, wstride); break;
+    default: factored_T<kPanelSlots, false>(v, P, T, SEG, lane, w0, wstride); break;
   }
 }
 
 // AP = diag P - A T over elements e0, e0 + estride, ...; accumulates (p.Ap, px.p) when part != nullptr.
+// Laplacian splitting (ldm != nullptr, DG = s): AP = s P - (A T + b (x) sum_j A_ij (P[j][l] - P[i][l]))
+// with T from factored_T<LAP> and b = ldm = d' - q' of the L nodes.
 __device__ void factored_AP(const PairView& v, const float* P, const float* T, float* AP, const float* DG,
-                            int64_t e0, int64_t estride, const float* pu, const float* pl, double2* part) {
+                            int64_t e0, int64_t estride, const float* pu, const float* pl, double2* part,
+                            const float* ldm) {
   const int m = v.m;
   const int64_t nm = (int64_t)v.n * m;
   const int64_t di = estride / m, dl = estride % m;
@@ -311,9 +382,21 @@ __device__ void factored_AP(const PairView& v, const float* P, const float* T, f
   double pap = 0.0, pxp = 0.0;
   for (int64_t e = e0; e < nm; e += estride) {
     float acc = 0.0f;
-    for (int k = v.urp[i]; k < v.urp[i + 1]; ++k) {
-      const float4 u = v.ue[k];
-      acc = fmaf(u.y, T[(int64_t)__float_as_int(u.x) * m + l], acc);
+    if (ldm) {
+      const float pi = P[e];
+      float acc2 = 0.0f;
+      for (int k = v.urp[i]; k < v.urp[i + 1]; ++k) {
+        const float4 u = v.ue[k];
+        const int64_t f = (int64_t)__float_as_int(u.x) * m + l;
+        acc = fmaf(u.y, T[f], acc);
+        acc2 = fmaf(u.y, P[f] - pi, acc2);
+      }
+      acc = fmaf(ldm[l], acc2, acc);
+    } else {
+      for (int k = v.urp[i]; k < v.urp[i + 1]; ++k) {
+        const float4 u = v.ue[k];
+        acc = fmaf(u.y, T[(int64_t)__float_as_int(u.x) * m + l], acc);
+      }
     }
     const float p = P[e];
     const float ap = fmaf(DG[e], p, -acc);
@@ -359,7 +442,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
   int32_t* c_lrp = c_urp + kCacheRows + 1;
   float* svec = psm + kPW * kSegFloats + kCacheFloats;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
-  const int64_t vstride = slab / 6;
+  const int64_t vstride = slab / kSlabVectors;
 
   for (;;) {
     if (threadIdx.x == 0) sh_pid = atomicAdd(queue, 1ull);
@@ -378,6 +461,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     const int n = U.n, m = L.n, nm = n * m;
     const int SL = 2 * L.ne;
     const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : kPanelSlots);
+    const bool lap = EK == KK_NONE && laplacian_pair(prm, U, L);
 
     PairView v;
     v.urp = ds.rowptr + U.rowptr_off;
@@ -426,6 +510,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     float* P = base + 3 * vstride;
     float* AP = base + 4 * vstride;
     float* T = base + 5 * vstride;  // unlabeled: P B^T
+    float* SD = base + 6 * vstride;  // Laplacian splitting: s = diag - rowsum(L)
     if (2 * nm <= smem_vec) {
       P = svec;
       AP = svec + nm;
@@ -435,11 +520,11 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     // ---- setup (solver.py:69-74, 91-97): diag, b, x = 0, r = b, z = r / diag, p = z
     double2 acc = make_double2(0.0, 0.0);
     for (int i = threadIdx.x; i < n; i += kPT) {
-      const double dq = ds.deg[U.node_off + i] * (double)ds.q[U.node_off + i];
+      const double dq = ds.deg[U.node_off + i] * ds.q64[U.node_off + i];
       acc.x += dq * dq;
     }
     for (int i = threadIdx.x; i < m; i += kPT) {
-      const double dq = ds.deg[L.node_off + i] * (double)ds.q[L.node_off + i];
+      const double dq = ds.deg[L.node_off + i] * ds.q64[L.node_off + i];
       acc.y += dq * dq;
     }
     int flip = 0;
@@ -453,11 +538,13 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
         const int64_t vu = U.node_off + i, vl = L.node_off + l;
         float kv = 1.0f;
         if (vlab)
-          kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
-                                ds.nl_kind == LK_CAT), prm.v_min);
-        const float dg = (float)(ds.deg[vu] * ds.deg[vl] / (double)kv);
-        const float b = (float)((ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]));
+          kv = floor_kv(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
+                                   ds.nl_kind == LK_CAT), prm, out);
+        const double dg64 = ds.deg[vu] * ds.deg[vl] / (double)kv;
+        const float dg = (float)dg64;
+        const float b = (float)((ds.deg[vu] * ds.q64[vu]) * (ds.deg[vl] * ds.q64[vl]));
         const float z = b * rcp_approx(dg);
+        if (lap) SD[e] = (float)(dg64 - (ds.deg[vu] - ds.q64[vu]) * (ds.deg[vl] - ds.q64[vl]));
         DG[e] = dg;
         R[e] = b;
         P[e] = z;
@@ -487,13 +574,13 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     while (!conv && it < max_iter) {
       double2 part = make_double2(0.0, 0.0);
       if (EK == KK_NONE && factor) {
-        factored_T_dispatch(ns, v, P, T, SEG, lane, warp, kPW);
+        factored_T_dispatch(ns, v, P, T, SEG, lane, warp, kPW, lap);
         __syncthreads();
-        factored_AP(v, P, T, AP, DG, threadIdx.x, kPT, ds.p + U.node_off, ds.p + L.node_off,
-                    self_pair ? nullptr : &part);
+        factored_AP(v, P, T, AP, lap ? SD : DG, threadIdx.x, kPT, ds.p + U.node_off, ds.p + L.node_off,
+                    self_pair ? nullptr : &part, lap ? ds.dm + L.node_off : nullptr);
       } else {
-        xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, warp, kPW, ds.p + U.node_off, ds.p + L.node_off,
-                         self_pair ? nullptr : &part);
+        xmv_dispatch<EK>(ns, ek, v, P, AP, lap ? SD : DG, SEG, lane, warp, kPW, ds.p + U.node_off,
+                         ds.p + L.node_off, self_pair ? nullptr : &part, lap);
       }
       __syncthreads();
       if (self_pair) {
@@ -712,6 +799,7 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
   float* P = vec + 3 * vstride;
   float* AP = vec + 4 * vstride;
   float* T = vec + 5 * vstride;  // unlabeled: P B^T
+  float* SD = vec + 6 * vstride;  // Laplacian splitting: s = diag - rowsum(L)
   int flip = 0;
   auto gsum = [&](double2 v) {
     double2 r = grid_sum2(v, gbuf + flip * gridDim.x, wred, &sres, grid);
@@ -731,6 +819,7 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     const int n = U.n, m = L.n, nm = n * m;
     const int SL = 2 * L.ne;
     const int ns = SL <= 64 ? 2 : (SL <= 128 ? 4 : kPanelSlots);
+    const bool lap = EK == KK_NONE && laplacian_pair(prm, U, L);
     PairView v;
     v.urp = ds.rowptr + U.rowptr_off;
     v.ue = ds.rowent + U.nz_off;
@@ -745,11 +834,11 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
 
     double2 acc = make_double2(0.0, 0.0);
     for (int64_t i = gtid; i < n; i += gthreads) {
-      const double dq = ds.deg[U.node_off + i] * (double)ds.q[U.node_off + i];
+      const double dq = ds.deg[U.node_off + i] * ds.q64[U.node_off + i];
       acc.x += dq * dq;
     }
     for (int64_t i = gtid; i < m; i += gthreads) {
-      const double dq = ds.deg[L.node_off + i] * (double)ds.q[L.node_off + i];
+      const double dq = ds.deg[L.node_off + i] * ds.q64[L.node_off + i];
       acc.y += dq * dq;
     }
     double2 s = gsum(acc);
@@ -761,11 +850,13 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
         const int64_t vu = U.node_off + i, vl = L.node_off + l;
         float kv = 1.0f;
         if (vlab)
-          kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
-                                ds.nl_kind == LK_CAT), prm.v_min);
-        const float dg = (float)(ds.deg[vu] * ds.deg[vl] / (double)kv);
-        const float b = (float)((ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]));
+          kv = floor_kv(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
+                                   ds.nl_kind == LK_CAT), prm, out);
+        const double dg64 = ds.deg[vu] * ds.deg[vl] / (double)kv;
+        const float dg = (float)dg64;
+        const float b = (float)((ds.deg[vu] * ds.q64[vu]) * (ds.deg[vl] * ds.q64[vl]));
         const float z = b * rcp_approx(dg);
+        if (lap) SD[e] = (float)(dg64 - (ds.deg[vu] - ds.q64[vu]) * (ds.deg[vl] - ds.q64[vl]));
         DG[e] = dg;
         R[e] = b;
         P[e] = z;
@@ -792,13 +883,13 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     while (!conv && it < max_iter) {
       double2 part = make_double2(0.0, 0.0);
       if (EK == KK_NONE && factor) {
-        factored_T_dispatch(ns, v, P, T, SEG, lane, gw, GW);
+        factored_T_dispatch(ns, v, P, T, SEG, lane, gw, GW, lap);
         grid.sync();
-        factored_AP(v, P, T, AP, DG, gtid, gthreads, ds.p + U.node_off, ds.p + L.node_off,
-                    self_pair ? nullptr : &part);
+        factored_AP(v, P, T, AP, lap ? SD : DG, gtid, gthreads, ds.p + U.node_off, ds.p + L.node_off,
+                    self_pair ? nullptr : &part, lap ? ds.dm + L.node_off : nullptr);
       } else {
-        xmv_dispatch<EK>(ns, ek, v, P, AP, DG, SEG, lane, gw, GW, ds.p + U.node_off, ds.p + L.node_off,
-                         self_pair ? nullptr : &part);
+        xmv_dispatch<EK>(ns, ek, v, P, AP, lap ? SD : DG, SEG, lane, gw, GW, ds.p + U.node_off,
+                         ds.p + L.node_off, self_pair ? nullptr : &part, lap);
       }
       if (self_pair) {
         grid.sync();

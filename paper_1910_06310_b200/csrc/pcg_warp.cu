@@ -56,6 +56,7 @@ struct WarpSmem {
   int lrow[40];
   float upq[NU];          // p_i of U nodes
   float udq[NU];          // d_i q_i of U nodes
+  float udm[UNLAB ? NU : 1];  // d_i - q_i of U nodes (Laplacian splitting: preconditioner = s + udm * ldm)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -100,12 +101,17 @@ __device__ __forceinline__ void write_pair_outputs(const SolveOut& out, unsigned
 // diag[i][l] = d_i d'_l / max(kv, v_min)  (product.py:164-178, 210); kept out of
 // line so the vertex-kernel code exists once per kernel (instruction-cache footprint)
 __device__ __noinline__ double diag_of(const DatasetDev& ds, const KernelDesc& vk, const SolveParams& prm,
-                                          bool vlab, int64_t vu, int64_t vl) {
+                                       const SolveOut& out, bool vlab, int64_t vu, int64_t vl) {
   float kv = 1.0f;
   if (vlab)
-    kv = fmaxf(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
-                          ds.nl_kind == LK_CAT), prm.v_min);
+    kv = floor_kv(kernel_vec(vk, ds.vlabel + vu * ds.nl_dim, ds.vlabel + vl * ds.nl_dim, ds.nl_dim,
+                             ds.nl_kind == LK_CAT), prm, out);
   return ds.deg[vu] * ds.deg[vl] / (double)kv;
+}
+
+// s = diag - rowsum(L) for kappa_e = 1: rowsum = (d - q)(d' - q'), both in FP64 (Laplacian splitting)
+__device__ __forceinline__ double shifted_diag(const DatasetDev& ds, double diag, int64_t vu, int64_t vl) {
+  return diag - (ds.deg[vu] - ds.q64[vu]) * (ds.deg[vl] - ds.q64[vl]);
 }
 
 // ---------------------------------------------------------------------------
@@ -119,20 +125,22 @@ constexpr int kTinyMax = 128;
 
 template <int EK>
 __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
-                           const GraphDesc& U, const GraphDesc& L, const float2* uwl, const int* uoff,
-                           const int* urow, const float4* le, const int* lrow, double* P, double* AP, double* DG,
-                           int lane, double& value_out, int64_t& it_out, bool& conv_out, double& rr_out, float* nw,
-                           bool swap) {
+                           const SolveOut& out, const GraphDesc& U, const GraphDesc& L, const float2* uwl,
+                           const int* uoff, const int* urow, const float4* le, const int* lrow, double* P, double* AP,
+                           double* DG, double* SS, int lane, double& value_out, int64_t& it_out, bool& conv_out,
+                           double& rr_out, float* nw, bool swap) {
   const int nu = U.n, m = L.n, nm = nu * m;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
+  // kappa_e = 1 with a large diag / s: A p = s p - sum c (p_j - p_i), s in FP64 (mgk_dev.cuh kLapFactor)
+  const bool lap = EK == KK_NONE && laplacian_pair(prm, U, L);
   double r[4], x[4];
   double bb_u = 0.0, bb_l = 0.0;
   if (lane < nu) {
-    double dq = ds.deg[U.node_off + lane] * (double)ds.q[U.node_off + lane];
+    double dq = ds.deg[U.node_off + lane] * ds.q64[U.node_off + lane];
     bb_u = dq * dq;
   }
   if (lane < m) {
-    double dq = ds.deg[L.node_off + lane] * (double)ds.q[L.node_off + lane];
+    double dq = ds.deg[L.node_off + lane] * ds.q64[L.node_off + lane];
     bb_l = dq * dq;
   }
   double rho = 0.0, rr = 0.0;
@@ -144,9 +152,10 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
     if (e < nm) {
       const int i = e / m, l = e - i * m;
       const int64_t vu = U.node_off + i, vl = L.node_off + l;
-      const double dg = diag_of(ds, vk, prm, vlab, vu, vl);
-      const double b = (ds.deg[vu] * (double)ds.q[vu]) * (ds.deg[vl] * (double)ds.q[vl]);
+      const double dg = diag_of(ds, vk, prm, out, vlab, vu, vl);
+      const double b = (ds.deg[vu] * ds.q64[vu]) * (ds.deg[vl] * ds.q64[vl]);
       DG[e] = dg;
+      SS[e] = lap ? shifted_diag(ds, dg, vu, vl) : dg;
       r[s] = b;
       const double z = b / dg;
       P[e] = z;
@@ -167,6 +176,7 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       const int e = lane + 32 * s;
       if (e < nm) {
         const int i = e / m, l = e - i * m;
+        const double pc = lap ? P[e] : 0.0;
         double acc = 0.0;
         for (int k = urow[i]; k < urow[i + 1]; ++k) {
           const float2 a = uwl[k];
@@ -174,10 +184,10 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
           for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
             const float4 b = le[q];
             const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
-            acc = fma((double)c, prow[__float_as_int(b.x)], acc);
+            acc = fma((double)c, prow[__float_as_int(b.x)] - pc, acc);
           }
         }
-        AP[e] = DG[e] * P[e] - acc;
+        AP[e] = SS[e] * P[e] - acc;
       }
     }
     __syncwarp();
@@ -303,14 +313,23 @@ __device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int n
 }
 
 // XMV, unlabeled (kappa = 1): T = P B^T (slots + segment sums), OFF = A T.
-template <int NS, int SLM, class Smem>
+// LAP (Laplacian splitting, mgk_dev.cuh kLapFactor): OFF = sum L (p_jj' - p_ii') instead, in the same
+// factorised form via p_jj' - p_ii' = (p_jj' - p_ji') + (p_ji' - p_ii'):
+//   T[j][i'] = sum_j' B_i'j' (p_jj' - p_ji'),  OFF[i][i'] = sum_j A_ij T[j][i'] + b_i' sum_j A_ij (p_ji' - p_ii')
+// with b_i' = d'_i' - q'_i' (a coefficient of differences: its FP32 rounding is harmless).
+template <int NS, int SLM, bool LAP, class Smem>
 __device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, const int (&lcoff)[SLM],
-                                              const float (&lw)[SLM], int lr0, int lr1) {
+                                              const float (&lw)[SLM], const int (&lroff)[SLM], int lr0, int lr1,
+                                              float lbm) {
   const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
   for (int j = 0; j < nu; ++j) {
     const char* row = pbase + j * 128;
 #pragma unroll
-    for (int t = 0; t < NS; ++t) S.SEG[lane + 32 * t] = lw[t] * *reinterpret_cast<const float*>(row + lcoff[t]);
+    for (int t = 0; t < NS; ++t) {
+      float v = *reinterpret_cast<const float*>(row + lcoff[t]);
+      if constexpr (LAP) v -= *reinterpret_cast<const float*>(row + lroff[t]);
+      S.SEG[lane + 32 * t] = lw[t] * v;
+    }
     __syncwarp();
     if (lane < m) {
       float s = 0.0f;
@@ -321,12 +340,15 @@ __device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, 
     __syncwarp();
   }
   for (int i = 0; i < nu; ++i) {
-    float s = 0.0f;
+    float s = 0.0f, s2 = 0.0f;
+    const float pi = LAP ? S.P[i][lane] : 0.0f;
     for (int k = S.urow[i]; k < S.urow[i + 1]; ++k) {
       const float4 e = S.UE[k];
-      s = fmaf(e.x, S.T[__float_as_int(e.z) >> 7][lane], s);
+      const int j = __float_as_int(e.z) >> 7;
+      s = fmaf(e.x, S.T[j][lane], s);
+      if constexpr (LAP) s2 = fmaf(e.x, S.P[j][lane] - pi, s2);
     }
-    if (lane < m) S.OFF[i][lane] = s;
+    if (lane < m) S.OFF[i][lane] = LAP ? fmaf(lbm, s2, s) : s;
   }
   __syncwarp();
 }
@@ -334,15 +356,20 @@ __device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, 
 template <int EK, int SLM, class Smem>
 __device__ __forceinline__ void xmv_dispatch(int ns, Smem& S, const KernelDesc& ek, int nu, int m, int lane,
                                              const int (&lcoff)[SLM], const float (&lw)[SLM],
-                                             const float (&llab)[SLM], int lr0, int lr1) {
-#define MGK_XMV_CASE(N)                                                          \
-  case N:                                                                        \
-    if constexpr (N <= SLM) {                                                    \
-      if constexpr (EK == KK_NONE)                                               \
-        xmv_unlabeled<N, SLM>(S, nu, m, lane, lcoff, lw, lr0, lr1);              \
-      else                                                                       \
-        xmv_labeled<N, EK, SLM>(S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);  \
-    }                                                                            \
+                                             const float (&llab)[SLM], const int (&lroff)[SLM], int lr0, int lr1,
+                                             bool lap, float lbm) {
+#define MGK_XMV_CASE(N)                                                                  \
+  case N:                                                                                \
+    if constexpr (N <= SLM) {                                                            \
+      if constexpr (EK == KK_NONE) {                                                     \
+        if (lap)                                                                         \
+          xmv_unlabeled<N, SLM, true>(S, nu, m, lane, lcoff, lw, lroff, lr0, lr1, lbm);  \
+        else                                                                             \
+          xmv_unlabeled<N, SLM, false>(S, nu, m, lane, lcoff, lw, lroff, lr0, lr1, lbm); \
+      } else {                                                                           \
+        xmv_labeled<N, EK, SLM>(S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);          \
+      }                                                                                  \
+    }                                                                                    \
     break;
   switch (ns) {
     MGK_XMV_CASE(1)
@@ -422,12 +449,13 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       if (lane <= m) S.lrow[lane] = ds.rowptr[L.rowptr_off + lane];
     }
     __syncwarp();
-    int lcoff[SLM];
+    int lcoff[SLM], lroff[SLM];
     float lw[SLM], llab[SLM];
 #pragma unroll
     for (int t = 0; t < SLM; ++t) {
       const int k = lane + 32 * t;
       lcoff[t] = 0;
+      lroff[t] = 0;
       lw[t] = 0.0f;
       llab[t] = 0.0f;
       if (k < SL) {
@@ -435,6 +463,11 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
         lcoff[t] = __float_as_int(e.x) * 4;
         lw[t] = e.y;
         llab[t] = e.z;
+        if constexpr (UNLAB) {  // L row of the slot (Laplacian splitting)
+          int r = 0;
+          while (S.lrow[r + 1] <= k) ++r;
+          lroff[t] = r * 4;
+        }
       }
     }
     int lr0 = 0, lr1 = 0;
@@ -447,18 +480,22 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
 
     // ---- node data: L on lanes, U in shared memory; vectors as [U node][lane]
     double ldq = 0.0;
-    float lp = 0.0f;
+    float lp = 0.0f, lbm = 0.0f;
     if (lane < m) {
       const int64_t v = L.node_off + lane;
-      ldq = ds.deg[v] * (double)ds.q[v];
+      ldq = ds.deg[v] * ds.q64[v];
       lp = ds.p[v];
+      lbm = ds.dm[v];
     }
+    // kappa_e = 1 pairs with a large diag / s: Laplacian splitting (dv = s, preconditioner s + udm lbm)
+    const bool lap = UNLAB && laplacian_pair(prm, U, L);
     double bb_u = 0.0;
     if (lane < nu) {
       const int64_t v = U.node_off + lane;
-      const double dq = ds.deg[v] * (double)ds.q[v];
+      const double dq = ds.deg[v] * ds.q64[v];
       S.udq[lane] = (float)dq;
       S.upq[lane] = ds.p[v];
+      if constexpr (UNLAB) S.udm[lane] = ds.dm[v];
       bb_u = dq * dq;
     }
     // b = (d q) (x) (d' q');  eps = tol^2 b.b  (solver.py:69-74, 88) -- b.b is separable
@@ -488,15 +525,17 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       if (i < nu) {
         float p0 = 0.0f;
         if (active) {
+          const int64_t vu = U.node_off + i, vl = L.node_off + lane;
+          double dg;
           if (vfast) {
-            const int64_t vu = U.node_off + i;
             const bool same = !vlab || __float_as_int(ds.vlabel[vu]) == llabel;
-            dv[i] = (float)(ds.deg[vu] * ldeg * (same ? 1.0 : inv_h));
+            dg = ds.deg[vu] * ldeg * (same ? 1.0 : inv_h);
           } else {
-            dv[i] = (float)diag_of(ds, vk, prm, vlab, U.node_off + i, L.node_off + lane);
+            dg = diag_of(ds, vk, prm, out, vlab, vu, vl);
           }
+          dv[i] = (float)(lap ? shifted_diag(ds, dg, vu, vl) : dg);
           rv[i] = (float)((double)S.udq[i] * ldq);
-          p0 = rv[i] * rcp_approx(dv[i]);
+          p0 = rv[i] * rcp_approx((float)dg);
           rho += (double)rv[i] * (double)p0;
           rr += (double)rv[i] * (double)rv[i];
         }
@@ -514,7 +553,7 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
 
     while (!conv && it < max_iter) {
       // ---------------- off-diagonal product OFF = (A (x) A' . ke) P
-      xmv_dispatch<EK, SLM>(ns, S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);
+      xmv_dispatch<EK, SLM>(ns, S, ek, nu, m, lane, lcoff, lw, llab, lroff, lr0, lr1, lap, lbm);
       if (self_pair) {
         // self pair: the exact operator maps symmetric fields to symmetric fields;
         // symmetrising keeps the FP32 Krylov space in that subspace as the FP64
@@ -552,7 +591,8 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
         if (active) {
           if constexpr (NODEWISE) S.X[i][lane] = fmaf(af, S.P[i][lane], S.X[i][lane]);
           const float r = fmaf(-af, S.OFF[i][lane], rv[i]);
-          const float z = r * rcp_approx(dv[i]);
+          // preconditioner: the full diagonal (Laplacian splitting: s + (d - q)(d' - q'))
+          const float z = r * rcp_approx(UNLAB && lap ? fmaf(S.udm[i], lbm, dv[i]) : dv[i]);
           rv[i] = r;
           S.OFF[i][lane] = z;
           rr_l += (double)r * (double)r;
@@ -594,7 +634,7 @@ struct TinySmem {
   float2 UWL[SMAX];
   int UOFF[SMAX];
   float4 LE[SMAX];
-  double V[3 * kTinyMax];  // P, AP, DG
+  double V[4 * kTinyMax];  // P, AP, DG, SS
   int urow[NU + 8];
   int lrow[40];
 };
@@ -633,8 +673,8 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int64_t it;
     bool conv;
     float* nw = out.nodewise ? out.nodewise + out.nodewise_off[pid] : nullptr;
-    solve_tiny<EK>(ds, vk, ek, prm, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.V, S.V + kTinyMax,
-                   S.V + 2 * kTinyMax, lane, val, it, conv, rr, nw, false);
+    solve_tiny<EK>(ds, vk, ek, prm, out, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.V, S.V + kTinyMax,
+                   S.V + 2 * kTinyMax, S.V + 3 * kTinyMax, lane, val, it, conv, rr, nw, false);
     write_pair_outputs(out, pid, ga, gb, val, it, conv, rr, lane);
     __syncwarp();
   }

@@ -164,7 +164,8 @@ __global__ void k_seg_emit(int64_t nseg, const int64_t* __restrict__ seg_start, 
 // d_i = (sum_j w_ij accumulated in ascending column order) + q_i  (graphs.py:202-214)
 __global__ void k_degrees(int64_t ntotal, const int32_t* __restrict__ node_graph, const GraphDesc* __restrict__ graphs,
                           const Octile* __restrict__ tiles, const int32_t* __restrict__ trow,
-                          const float* __restrict__ nz_w, const double* __restrict__ q64, double* __restrict__ deg) {
+                          const float* __restrict__ nz_w, const double* __restrict__ q64, double* __restrict__ deg,
+                          float* __restrict__ dm) {
   int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (v >= ntotal) return;
   const GraphDesc g = graphs[node_graph[v]];
@@ -180,6 +181,7 @@ __global__ void k_degrees(int64_t ntotal, const int32_t* __restrict__ node_graph
     for (int c = 0; byte; ++c, byte &= byte - 1) s += (double)w[c];
   }
   deg[v] = s + q64[v];
+  dm[v] = (float)s;  // d_i - q_i: the weight row sum (Laplacian splitting, mgk_dev.cuh)
 }
 
 // Exclusive scan of an int32 array into int64 (single CTA, chunked; n is the segment count).

@@ -28,6 +28,7 @@ SIGNATURES = {
     "mgk_ctx_destroy": (C.c_int, [_P]),
     "mgk_upload": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, C.c_int, C.c_int, _P, C.c_int, C.c_int, _P]),
     "mgk_set_kernels": (C.c_int, [_P, C.c_char_p, C.c_char_p]),
+    "mgk_set_vertex_floor": (C.c_int, [_P, C.c_double]),
     "mgk_reorder": (C.c_int, [_P, C.c_int, C.c_uint64, C.c_int, _P]),
     "mgk_tiles": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, _P]),
     "mgk_degrees": (C.c_int, [_P, C.c_int32, _P]),
@@ -128,6 +129,9 @@ class Context:
 
     def set_kernels(self, vspec: str | None, espec: str | None):
         check(self.lib.mgk_set_kernels(self.h, (vspec or "").encode(), (espec or "").encode()))
+
+    def set_vertex_floor(self, v_min: float):
+        check(self.lib.mgk_set_vertex_floor(self.h, float(v_min)))
 
     def reorder_pbr(self, seed: int, apply: bool) -> np.ndarray:
         out = np.empty(int(self.packed.node_off[-1]), dtype=np.int64)

@@ -109,6 +109,7 @@ def kernel(g_a: LabeledGraph, g_b: LabeledGraph, vertex_kernel=None, edge_kernel
     with _ctx_lock:
         ctx.upload(native.PackedDataset([g_a, g_b]))
         ctx.set_kernels(kernel_spec(vk), kernel_spec(ek))
+        ctx.set_vertex_floor(cfg.v_min)
         perm = None
         if reorder == "pbr":
             perm = ctx.reorder_pbr(seed, apply=True)
