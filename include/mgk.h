@@ -32,7 +32,7 @@ enum {
 /* label kinds (graphs.py:126-146) */
 enum { MGK_LABEL_NONE = 0, MGK_LABEL_CATEGORICAL = 1, MGK_LABEL_VECTOR = 2 };
 /* reorder methods (solver.py:209, 249-259) */
-enum { MGK_REORDER_NONE = 0, MGK_REORDER_PBR = 1 };
+enum { MGK_REORDER_NONE = 0, MGK_REORDER_PBR = 1, MGK_REORDER_RCM = 2, MGK_REORDER_MORTON = 3 };
 
 /* Version string of the library build. */
 const char* mgk_version(void);
@@ -71,8 +71,15 @@ int mgk_set_kernels(mgk_ctx* ctx, const char* vertex_spec, const char* edge_spec
  * similarity".  Default 1e-12 (DEFAULT_VERTEX_FLOOR). */
 int mgk_set_vertex_floor(mgk_ctx* ctx, double v_min);
 
-/* Per-graph partition-based reordering on the device (pbr_reorder,
- * reorder.py:361-404), same seed for every graph (solver.py:236-237).
+/* Per-graph node reordering on the device (solver.py:249-259 _reorder_for),
+ * one method for every graph:
+ *   MGK_REORDER_PBR     pbr_reorder (reorder.py:361-404), same seed for every
+ *                       graph (solver.py:236-237);
+ *   MGK_REORDER_RCM     rcm_reorder (reorder.py:412-443), seed unused;
+ *   MGK_REORDER_MORTON  morton_reorder of the node coordinates (reorder.py:
+ *                       448-478): the dataset's vector node labels of
+ *                       dimension 2 or 3, else MGK_E_INVALID "morton
+ *                       reordering needs 2D/3D coordinate node labels".
  * Writes forward maps (old -> new) into perms_out[sum n] when non-NULL.  With
  * apply != 0 the dataset is relabelled (apply_permutation, reorder.py:86-109)
  * and its octiles rebuilt. */
@@ -146,6 +153,18 @@ int mgk_kernel(mgk_ctx* ctx, int32_t a, int32_t b, double tol, int64_t max_iter,
  * to size them, then again with buffers of edge_off[N] entries. */
 int mgk_spatial_edges(int device, int32_t N, const int64_t* node_off, int dim, const double* points, double cutoff,
                       int64_t* edge_off, int32_t* ei, int32_t* ej, double* w, double* d);
+
+/* Cost counters of the pair (a, b) after `applies` operator applications
+ * (ProductOperator.counter_report, product.py:212-272, 423-436; the solver
+ * applies the operator once per iteration, solver.py:98-99):
+ * model = {E, F, X, r} (CostModel, costs.py:27-43; tile size 8),
+ * thresholds = {sparse_min_max, sparse_max_max, dense_min}
+ * (SelectionThresholds, product.py:38-53), force_dense = the reference's
+ * force_dense_stream.  out = {flops, t1_load, t1_store, t2_load, t2_store,
+ * tile_pairs}, summed from the device octiles' per-graph density histograms
+ * (nonzeros per tile, non-empty tile rows). */
+int mgk_counters(mgk_ctx* ctx, int32_t a, int32_t b, int64_t applies, const double* model,
+                 const int32_t* thresholds, int force_dense, double* out);
 
 /* Device time (ms, CUDA events on the solver stream) and the number of
  * kernel launches of the last solve call. */

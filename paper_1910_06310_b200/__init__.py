@@ -9,11 +9,13 @@ host-side mirror of the reference interface.
 
 from .basekernels import (BaseKernel, CompactPolynomial, ConstantOne, KernelRangeError, KernelShapeError,
                           KroneckerDelta, ProductComposite, RConvolution, SquareExponential, kernel_from_spec)
+from .costs import CostModel, CounterReport, PRIMITIVES, SelectionThresholds, predict_costs, select_tile_kernel
 from .graphs import DEFAULT_STOP_PROB, LabeledGraph, ValidationReport, validate_graph
 from .graphio import PointCloud, spatial_graph, spatial_graphs
 from .gram import (GramResult, compute_gram, load_gram_binary, load_gram_csv, nodewise_gram, normalize_gram,
                    save_gram_binary, save_gram_csv, schedule_pairs, stream_nodewise)
-from .reorder import Permutation, apply_permutation, objective, partition_objective, pbr_reorder, pbr_reorder_many
+from .reorder import (Permutation, apply_permutation, morton_reorder, objective, partition_objective, pbr_reorder,
+                      pbr_reorder_many, rcm_reorder, rcm_reorder_many)
 from .solver import KernelResult, SolverConfig, kernel
 from .tiles import TILE_SIZE, Tile, TiledMatrix, TileHistogram, build_tiles, dump_tiles, expand_tile, tile_histogram
 

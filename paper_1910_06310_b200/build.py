@@ -16,7 +16,7 @@ HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libmgk.so"
 SOURCES = ["capi.cu", "tiles.cu", "pcg_warp.cu", "pcg_panel.cu", "pcg_block.cu", "pbr.cu", "bench_support.cu",
-           "gram_post.cu", "ingest.cu"]
+           "gram_post.cu", "ingest.cu", "order.cu"]
 # sources compiled more than once: (source, object stem, extra flags)
 VARIANTS = {"pcg_panel.cu": [("pcg_panel_256", ["-DMGK_PANEL_THREADS=256", "-DMGK_PANEL_NS=p256"]),
                              ("pcg_panel_512", ["-DMGK_PANEL_THREADS=512", "-DMGK_PANEL_NS=p512"])]}

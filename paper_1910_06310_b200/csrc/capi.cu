@@ -291,6 +291,8 @@ struct mgk_ctx {
   DBuf<float> d_dm;
   DBuf<int32_t> d_status;
   double v_min = 1e-12;  // SolverConfig.v_min (solver.py:39-52), mgk_set_vertex_floor
+  float max_dqr = 1.0f;  // largest GraphDesc::dqr of the dataset (precise-mode switch, kPreciseLap)
+  std::vector<int32_t> h_hist;  // k_tile_hist per graph (cost counters), filled on first use after prepare
   DBuf<int32_t> d_ei, d_ej, d_egraph, d_ngraph, d_trow, d_segcount, d_segcursor, d_segntiles, d_seggraph, d_segrow;
   DBuf<int64_t> d_gseg, d_segstart, d_segtile;
   DBuf<uint64_t> d_keys, d_keys2;
@@ -601,6 +603,7 @@ static int prepare(mgk_ctx* c) {
   for (int64_t i = 0; i < ne; ++i) w32[i] = (float)c->w[i];
   std::vector<GraphDesc> gd(G);
   std::vector<int32_t> rowptr(nn + G), panels;
+  c->max_dqr = 1.0f;
   int64_t trow_off = 0;
   for (int g = 0; g < G; ++g) {
     GraphDesc d{};
@@ -645,6 +648,7 @@ static int prepare(mgk_ctx* c) {
       d.dqr = (float)std::min(r, 3.0e38);
     }
     gd[g] = d;
+    c->max_dqr = std::max(c->max_dqr, d.dqr);
     for (int64_t i = c->node_off[g]; i < c->node_off[g + 1]; ++i) ngraph[i] = g;
     for (int64_t i = c->edge_off[g]; i < c->edge_off[g + 1]; ++i) egraph[i] = g;
   }
@@ -685,6 +689,7 @@ static int prepare(mgk_ctx* c) {
   ds.rowptr = c->d_rowptr.ptr;
   ds.rowent = c->d_rowent.ptr;
   ds.panel_row = c->d_panel.ptr;
+  c->h_hist.clear();
   c->prepared = true;
   return MGK_OK;
 }
@@ -754,6 +759,8 @@ static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   p.panel_rpc = getenv("MGK_PANEL_RPC") ? atoi(getenv("MGK_PANEL_RPC")) : 0;
   // product.py:153-161 with dataset-uniform label presence; kappa = 1 when ek is None/const1
   p.labeled = (c->el_kind != LK_NONE && c->espec.kind != KK_NONE && c->espec.kind != KK_CONST1) ? 1 : 0;
+  p.fp64 = (!p.labeled && (tol < kPreciseTol || c->max_dqr > 2.0f * kPreciseLap)) ? 1 : 0;
+  if (const char* e = getenv("MGK_FP64")) p.fp64 = atoi(e) ? 1 : 0;
   return p;
 }
 
@@ -798,11 +805,11 @@ static int large_n() {
 }
 
 // Per-CTA slab (floats) for the block kernel.
-static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl) {
+static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, int64_t sl, bool fp64) {
   int64_t el = c->ds.el_dim > 2 ? c->ds.el_dim : 0;
   // 6 vectors (P, AP, R, X, DG, SD); + 6 * 128 + 8: a pair with n m <= tiny_nm (<= 128) runs with FP64
-  // vectors (2 floats per element)
-  int64_t f = 6 * n * m + 6 * 128 + 8 + 8 + 4 * (su + sl) + el * (su + sl) + (n + m + 2) + 16;
+  // vectors (2 floats per element), every pair does in a precise solve
+  int64_t f = (fp64 ? 12 : 6) * n * m + 6 * 128 + 8 + 8 + 4 * (su + sl) + el * (su + sl) + (n + m + 2) + 16;
   return (f + 31) / 32 * 32;
 }
 
@@ -828,7 +835,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     JobSpec& j = jobs[k];
     if (j.job.npairs <= 0) continue;
     if (j.kernel == JK_BLOCK) {
-      slabs[k] = block_slab(c, j.max_n, j.max_m, j.max_su, j.max_sl);
+      slabs[k] = block_slab(c, j.max_n, j.max_m, j.max_su, j.max_sl, prm.fp64 != 0);
       ctas[k] = 2 * c->num_sms;
     } else if (j.kernel == JK_PANEL) {
       const int64_t nm = j.max_n * j.max_m;
@@ -937,12 +944,14 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
 //   c(u) = first column whose n_u * n_v <= tiny_nm into a main ragged job
 //   [warp kernel, FP32] and a tiny ragged job [tiny kernel, FP64];
 //   pairs with a larger graph: TRI(other) + RECT(other x small) [block kernel].
-static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
+static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveParams& prm) {
   std::vector<int32_t> small, mid, large;
-  const bool panel = panel_dataset(c);
+  // a precise solve (prm.fp64) runs every pair on the FP64 block solver: one mid triangle
+  const bool precise = prm.fp64 != 0;
+  const bool panel = !precise && panel_dataset(c);
   for (int g = 0; g < c->G; ++g) {
     const GraphDesc& d = c->graphs[g];
-    if (small_graph(c, d))
+    if (!precise && small_graph(c, d))
       small.push_back(g);
     else if (panel && d.n >= large_n())
       large.push_back(g);
@@ -1003,28 +1012,42 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
     scol[u] = (int32_t)lo;
     spre[u + 1] = spre[u] + (nmid - lo);
   }
+  // mid x small pairs: row u of the mid list pairs with small columns [0, x(u)) on the CTA solver
+  // and [x(u), ns) -- n_u n_v <= tiny_nm, a dense small graph (n <= NU but too many nonzeros for the
+  // warp class) against a tiny partner -- on the block solver's FP64 vectors, the same predicate as
+  // mgk_pairs.  Mid graphs have n >= 19, so tiny partners have n <= 6 and lie in the narrow suffix.
+  std::vector<int64_t> rpre(nmid + 1, 0), xpre(nmid + 1, 0);
+  std::vector<int32_t> rcol(nmid), xcol(nmid);
+  for (int64_t u = 0; u < nmid; ++u) {
+    const int64_t nu = c->graphs[mid[u]].n;
+    int64_t lo = P, hi = ns;
+    while (lo < hi) {
+      const int64_t md = (lo + hi) / 2;
+      if ((int64_t)c->graphs[small[md]].n * nu > T) lo = md + 1; else hi = md;
+    }
+    rcol[u] = (int32_t)nmid;  // columns index the combined [mid ++ small] list
+    rpre[u + 1] = rpre[u] + lo;
+    xcol[u] = (int32_t)(nmid + lo);
+    xpre[u + 1] = xpre[u] + (ns - lo);
+  }
   cudaStream_t s = c->stream;
-  std::vector<int32_t> lists;  // small, mid, large
-  lists.insert(lists.end(), small.begin(), small.end());
-  lists.insert(lists.end(), mid.begin(), mid.end());
+  std::vector<int32_t> lists;  // large, mid, small (mid ++ small contiguous for the ragged mid x small jobs)
   lists.insert(lists.end(), large.begin(), large.end());
+  lists.insert(lists.end(), mid.begin(), mid.end());
+  lists.insert(lists.end(), small.begin(), small.end());
   CUDA_TRY(c->d_list_a.upload(lists, s));
   std::vector<int64_t> pre(mpre);
-  pre.insert(pre.end(), tpre.begin(), tpre.end());
-  pre.insert(pre.end(), bpre.begin(), bpre.end());
-  pre.insert(pre.end(), spre.begin(), spre.end());
+  for (auto* v : {&tpre, &bpre, &spre, &rpre, &xpre}) pre.insert(pre.end(), v->begin(), v->end());
   std::vector<int32_t> col(mcol);
-  col.insert(col.end(), tcol.begin(), tcol.end());
-  col.insert(col.end(), bcol.begin(), bcol.end());
-  col.insert(col.end(), scol.begin(), scol.end());
+  for (auto* v : {&tcol, &bcol, &scol, &rcol, &xcol}) col.insert(col.end(), v->begin(), v->end());
   CUDA_TRY(c->d_rowpre.upload(pre, s));
   CUDA_TRY(c->d_rowcol.upload(col, s));
   c->h_lists = lists;
   c->h_rowpre = pre;
   c->h_rowcol = col;
-  const int32_t* dsmall = c->d_list_a.ptr;
-  const int32_t* dmid = dsmall + ns;
-  const int32_t* dlarge = dmid + nmid;
+  const int32_t* dlarge = c->d_list_a.ptr;
+  const int32_t* dmid = dlarge + nl;
+  const int32_t* dsmall = dmid + nmid;
   auto mx = [c](const std::vector<int32_t>& vv, bool nodes) {
     int64_t r = 0;
     for (int32_t g : vv) r = std::max<int64_t>(r, nodes ? c->graphs[g].n : 2 * c->graphs[g].ne);
@@ -1074,52 +1097,16 @@ static int gram_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs) {
   } else {
     jms.job.npairs = 0;
   }
+  JobSpec jr = rect(mid, dmid, small, dsmall, cta), jx = rect(mid, dmid, small, dsmall, JK_BLOCK);
+  {
+    const int64_t* rp = c->d_rowpre.ptr + 2 * (ns + 1) + 2 * (nmid + 1);
+    const int32_t* rc = c->d_rowcol.ptr + 2 * ns + 2 * nmid;
+    jr.job = PairJob{PM_RAGGED, (int32_t)nmid, 0, rpre[nmid], 0, 1, dmid, nullptr, rp, rc};
+    jx.job = PairJob{PM_RAGGED, (int32_t)nmid, 0, xpre[nmid], 0, 1, dmid, nullptr, rp + nmid + 1, rc + nmid};
+  }
   // big pairs first (longest job first across classes)
   jobs = {tri(large, dlarge, JK_GRID), rect(large, dlarge, mid, dmid, cta), rect(large, dlarge, small, dsmall, cta),
-          jmb, jms, rect(mid, dmid, small, dsmall, cta), jw, jm, jt};
-  return MGK_OK;
-}
-
-// Gram fix-up pass: a graph of at most NU nodes that is outside the warp class (more than SMAX
-// nonzeros, e.g. a complete K20) lands in the mid list, so its pairs with n m <= tiny_nm ran FP32 on the
-// panel kernel.  They are re-solved on the block kernel's FP64 vectors (same canonical a <= b
-// orientation), overwriting the K entries; empty for datasets without such graphs.
-static int gram_fixup_job(mgk_ctx* c, JobSpec& j) {
-  j.job.npairs = 0;
-  if (!panel_dataset(c)) return MGK_OK;  // the block kernel already solved every pair
-  const int T = tiny_nm();
-  std::vector<char> dense(c->G, 0);
-  bool any = false;
-  for (int g = 0; g < c->G; ++g) {
-    const GraphDesc& d = c->graphs[g];
-    dense[g] = d.n <= SmallClass::NU && !small_graph(c, d) && (int64_t)d.n <= T;
-    any = any || dense[g];
-  }
-  if (!any) return MGK_OK;
-  std::vector<int32_t> la, lb;
-  int64_t mn = 0, mm = 0, su = 0, sl = 0;
-  for (int g = 0; g < c->G; ++g) {
-    if (!dense[g]) continue;
-    for (int h = 0; h < c->G; ++h) {
-      if (dense[h] && h < g) continue;  // dense x dense pairs once
-      if ((int64_t)c->graphs[g].n * c->graphs[h].n > T) continue;
-      const int32_t a = std::min(g, h), b = std::max(g, h);
-      la.push_back(a);
-      lb.push_back(b);
-      mn = std::max<int64_t>(mn, c->graphs[a].n);
-      mm = std::max<int64_t>(mm, c->graphs[b].n);
-      su = std::max<int64_t>(su, 2 * c->graphs[a].ne);
-      sl = std::max<int64_t>(sl, 2 * c->graphs[b].ne);
-    }
-  }
-  CUDA_TRY(c->d_list_b.upload(la, c->stream));
-  CUDA_TRY(c->d_list_c.upload(lb, c->stream));
-  j.job = PairJob{PM_LIST, 0, 0, (int64_t)la.size(), 0, 1, c->d_list_b.ptr, c->d_list_c.ptr, nullptr, nullptr};
-  j.kernel = JK_BLOCK;
-  j.max_n = mn;
-  j.max_m = mm;
-  j.max_su = su;
-  j.max_sl = sl;
+          jmb, jms, jr, jw, jm, jt, jx};
   return MGK_OK;
 }
 
@@ -1128,8 +1115,9 @@ int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters
   if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
   int rc = prepare(c);
   if (rc) return rc;
+  const SolveParams prm = make_params(c, tol, max_iter);
   std::vector<JobSpec> jobs;
-  rc = gram_jobs(c, jobs);
+  rc = gram_jobs(c, jobs, prm);
   if (rc) return rc;
   int64_t G = c->G;
   CUDA_TRY(c->d_K.alloc(G * G));
@@ -1141,18 +1129,8 @@ int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters
   o.K_conv = c->d_Kconv.ptr;
   o.G = G;
   std::vector<int64_t> offs(jobs.size(), 0);
-  rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
+  rc = run_jobs(c, jobs, o, offs, prm);
   if (rc) return rc;
-  std::vector<JobSpec> fix(1);
-  rc = gram_fixup_job(c, fix[0]);
-  if (rc) return rc;
-  if (fix[0].job.npairs > 0) {
-    const double ms = c->last_ms;
-    std::vector<int64_t> off1(1, 0);
-    rc = run_jobs(c, fix, o, off1, make_params(c, tol, max_iter));
-    if (rc) return rc;
-    c->last_ms += ms;
-  }
   if (K) CUDA_TRY(d2h(K, c->d_K.ptr, G * G * sizeof(double)));
   if (iters) CUDA_TRY(d2h(iters, c->d_Kit.ptr, G * G * sizeof(int32_t)));
   if (conv) CUDA_TRY(d2h(conv, c->d_Kconv.ptr, G * G));
@@ -1186,8 +1164,9 @@ int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter
   if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
   int rc = prepare(c);
   if (rc) return rc;
+  const SolveParams prm = make_params(c, tol, max_iter);
   std::vector<JobSpec> jobs;
-  rc = gram_jobs(c, jobs);
+  rc = gram_jobs(c, jobs, prm);
   if (rc) return rc;
   std::vector<int64_t> offs;
   int64_t total = 0;
@@ -1212,7 +1191,7 @@ int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter
   o.conv = c->d_conv.ptr;
   o.pair_a = c->d_pa.ptr;
   o.pair_b = c->d_pb.ptr;
-  rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
+  rc = run_jobs(c, jobs, o, offs, prm);
   if (rc) return rc;
   if (pair_a) CUDA_TRY(d2h(pair_a, c->d_pa.ptr, total * sizeof(int32_t)));
   if (pair_b) CUDA_TRY(d2h(pair_b, c->d_pb.ptr, total * sizeof(int32_t)));
@@ -1243,10 +1222,10 @@ int mgk_gram_nodewise(mgk_ctx* c, int rank, int world, double tol, int64_t max_i
   if (!sink) return fail(MGK_E_INVALID, "null sink");
   int rc = prepare(c);
   if (rc) return rc;
-  std::vector<JobSpec> jobs;
-  rc = gram_jobs(c, jobs);
-  if (rc) return rc;
   const SolveParams prm = make_params(c, tol, max_iter);
+  std::vector<JobSpec> jobs;
+  rc = gram_jobs(c, jobs, prm);
+  if (rc) return rc;
   int64_t max_pair = 0;
   for (const GraphDesc& d : c->graphs) max_pair = std::max<int64_t>(max_pair, d.n);
   max_pair *= max_pair;
@@ -1431,11 +1410,13 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
   std::vector<int32_t> ta, tb, wa, wb, ba, bb, ga_, gb_, xa, xb;
   std::vector<int64_t> tidx, widx, bidx, gidx, xidx;
   int64_t bn = 0, bm = 0, bsu = 0, bsl = 0, gn = 0, gm = 0, xn = 0, xm = 0, xsu = 0, xsl = 0;
-  const bool panel = panel_dataset(c);
+  const SolveParams prm = make_params(c, tol, max_iter);
+  const bool precise = prm.fp64 != 0;  // every pair on the FP64 block solver
+  const bool panel = !precise && panel_dataset(c);
   const int T = tiny_nm();
   for (int64_t k = 0; k < npairs; ++k) {
     const GraphDesc &A = c->graphs[a[k]], &B = c->graphs[b[k]];
-    if (small_graph(c, A) && small_graph(c, B)) {
+    if (!precise && small_graph(c, A) && small_graph(c, B)) {
       const bool tiny = (int64_t)A.n * B.n <= T;
       (tiny ? ta : wa).push_back(a[k]);
       (tiny ? tb : wb).push_back(b[k]);
@@ -1529,7 +1510,7 @@ int mgk_pairs(mgk_ctx* c, int64_t npairs, const int32_t* a, const int32_t* b, do
     o.nodewise = c->d_nodewise.ptr;
     o.nodewise_off = c->d_nwoff.ptr;
   }
-  rc = run_jobs(c, jobs, o, offs, make_params(c, tol, max_iter));
+  rc = run_jobs(c, jobs, o, offs, prm);
   if (rc) return rc;
   std::vector<double> hv(npairs);
   std::vector<int32_t> hi(npairs);
@@ -1566,6 +1547,72 @@ int mgk_kernel(mgk_ctx* c, int32_t a, int32_t b, double tol, int64_t max_iter, d
   return mgk_pairs(c, 1, &a, &b, tol, max_iter, value, iters, residual, conv, nodewise);
 }
 
+int mgk_counters(mgk_ctx* c, int32_t a, int32_t b, int64_t applies, const double* model, const int32_t* thresholds,
+                 int force_dense, double* out) {
+  if (!c || !model || !thresholds || !out) return fail(MGK_E_INVALID, "null argument");
+  if (applies < 0) return fail(MGK_E_INVALID, "applies must be >= 0");
+  int rc = prepare(c);
+  if (rc) return rc;
+  if (a < 0 || a >= c->G || b < 0 || b >= c->G) return fail(MGK_E_INVALID, "graph index out of range");
+  if (c->h_hist.empty()) {
+    DBuf<int32_t> d;
+    CUDA_TRY(d.alloc((size_t)c->G * kHistBins));
+    k_tile_hist<<<c->G, 128, 0, c->stream>>>(c->d_graphs.ptr, c->d_tiles.ptr, c->d_trow.ptr, d.ptr);
+    CUDA_TRY(cudaGetLastError());
+    c->h_hist.resize((size_t)c->G * kHistBins);
+    CUDA_TRY(cudaMemcpyAsync(c->h_hist.data(), d.ptr, c->h_hist.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  const int32_t* ha = c->h_hist.data() + (size_t)a * kHistBins;
+  const int32_t* hb = c->h_hist.data() + (size_t)b * kHistBins;
+  const double E = model[0], F = model[1], X = model[2], r = model[3], t = 8.0;
+  const int s1 = thresholds[0], s2 = thresholds[1], dmin = thresholds[2];
+  // per-apply increments of ProductOperator._build_plan (product.py:224-266), summed over the tile-pair
+  // density classes (na, nb) with multiplicity count_a[na] * count_b[nb]; every term is an integer, so the
+  // sums equal the reference's tile-pair-by-tile-pair accumulation exactly
+  double flops = 0, t1l = 0, t2l = 0, t2s = 0, pairs = 0;
+  for (int na = 1; na <= 64; ++na) {
+    if (!ha[na]) continue;
+    for (int nb = 1; nb <= 64; ++nb) {
+      if (!hb[nb]) continue;
+      const double mult = (double)ha[na] * (double)hb[nb];
+      pairs += mult;
+      if (force_dense) {
+        flops += mult * (t * t * t * t * X);
+        t1l += mult * (t * t * (E + 2 * F));
+        t2s += mult * (t * t * (E + F));
+        t2l += mult * (t * t * t * t * (E + F) * (1.0 / t + 1.0 / r));
+        continue;
+      }
+      t1l += mult * (8.0 + nb * (E + F) + t * t * F);
+      const int lo = std::min(na, nb), hi = std::max(na, nb);
+      double contrib;
+      if (lo <= s1 && hi <= s2) {  // select_tile_kernel (product.py:56-66)
+        contrib = (double)na * nb;
+        t2s += mult * ((na + nb) * (E + F));
+      } else if (lo >= dmin) {
+        contrib = t * t * t * t;
+        t2s += mult * (t * t * (E + F));
+      } else {
+        contrib = t * t * lo;
+        t2s += mult * (t * t * (E + F));
+      }
+      flops += mult * contrib * X;
+      t2l += mult * contrib * (E + 2 * F);
+    }
+  }
+  const double t1s = (double)ha[65] * (double)hb[65] * t * t * F;
+  const double k = (double)applies;
+  out[0] = k * flops;
+  out[1] = k * t1l;
+  out[2] = k * t1s;
+  out[3] = k * t2l;
+  out[4] = k * t2s;
+  out[5] = k * pairs;
+  return MGK_OK;
+}
+
 int mgk_transfer_bytes(int64_t* h2d, int64_t* d2h_out) {
   if (h2d) *h2d = g_h2d_bytes;
   if (d2h_out) *d2h_out = g_d2h_bytes;
@@ -1588,12 +1635,19 @@ int mgk_reorder(mgk_ctx* c, int method, uint64_t seed, int apply, int64_t* perms
         for (int64_t i = c->node_off[g]; i < c->node_off[g + 1]; ++i) perms_out[i] = i - c->node_off[g];
     return MGK_OK;
   }
-  if (method != MGK_REORDER_PBR) return fail(MGK_E_INVALID, "unknown reorder method %d", method);
-  int rc = prepare(c);  // octiles of the current order drive the tile-count fallback
+  if (method != MGK_REORDER_PBR && method != MGK_REORDER_RCM && method != MGK_REORDER_MORTON)
+    return fail(MGK_E_INVALID, "unknown reorder method %d", method);
+  if (method == MGK_REORDER_MORTON && !(c->nl_kind == LK_VEC && (c->nl_dim == 2 || c->nl_dim == 3)))
+    return fail(MGK_E_INVALID, "morton reordering needs 2D/3D coordinate node labels");
+  int rc = prepare(c);  // octiles of the current order drive the PBR tile-count fallback
   if (rc) return rc;
   std::vector<int64_t> fwd;
-  rc = pbr_device(c->G, c->node_off, c->edge_off, c->ei, c->ej, seed, c->d_tiles.ptr, c->graphs, c->d_trow.ptr,
-                  c->device, c->stream, fwd, g_err);
+  if (method == MGK_REORDER_PBR)
+    rc = pbr_device(c->G, c->node_off, c->edge_off, c->ei, c->ej, seed, c->d_tiles.ptr, c->graphs, c->d_trow.ptr,
+                    c->device, c->stream, fwd, g_err);
+  else
+    rc = order_device(method, c->G, c->graphs, c->d_graphs.ptr, c->d_ngraph.ptr, c->d_rowptr.ptr, c->d_rowent.ptr,
+                      c->nl_vec, c->nl_dim, c->stream, fwd, g_err);
   if (rc) return rc;
   if (perms_out) std::copy(fwd.begin(), fwd.end(), perms_out);
   if (apply) {

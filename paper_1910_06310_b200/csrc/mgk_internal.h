@@ -1,6 +1,8 @@
 // Internal declarations shared by the .cu translation units of libmgk.
 #pragma once
 #include <cstdint>
+#include <string>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "mgk_dev.cuh"
@@ -55,7 +57,20 @@ struct SolveParams {
   int32_t tiny_nm;          // n*m at or below which the warp solver runs the pair in FP64
   int32_t panel_rpc;        // U rows per panel work item (0: automatic)
   int32_t lap_mode;         // Laplacian splitting (kappa_e = 1 pairs): 0 off, 1 by factor, 2 always
+  int32_t fp64;             // every pair on the block solver with FP64 vectors (precise_tol)
 };
+
+// kappa_e = 1 systems solved to a relative residual below this bound run every pair with FP64
+// vectors on the block solver.  Unlabeled product graphs are highly structured: FP32 vectors cost
+// CG 3-8 extra iterations against the reference's float64 once the tolerance passes ~3e-7 (q = 5e-4)
+// and at 1e-10 for any q (emulation in tools/precision_emulate.py), while labeled
+// (kappa_e != 1) pairs keep iteration parity at the reference default 1e-10 in FP32.
+constexpr double kPreciseTol = 5e-7;
+// ... and so do kappa_e = 1 datasets whose largest self-pair cancellation factor max(d/q) / 2 exceeds
+// kPreciseLap (q below ~1e-3): there even the Laplacian-split FP32 iteration flips a +-1 iteration
+// count at tol 1e-6 (a q = 5e-4 self pair: 13 against the reference's 15).  Config-4 random geometric
+// graphs at q = 0.05 peak at 143 (mean degree 32) and stay on the FP32 solvers.
+constexpr float kPreciseLap = 256.0f;
 
 // Laplacian splitting for this pair (mgk_dev.cuh kLapFactor); only the kappa_e = 1 solvers read it.
 __host__ __device__ inline bool laplacian_pair(const SolveParams& prm, const GraphDesc& a, const GraphDesc& b) {
@@ -133,6 +148,8 @@ __global__ void k_trow(int, const int64_t*, const int64_t*, GraphDesc*, int32_t*
 __global__ void k_rows_fill(int64_t, const int32_t*, const GraphDesc*, const Octile*, const int32_t*, const float*,
                             const float*, int, const int32_t*, float4*);
 constexpr int kSortSmemBytes = 8192 * 8;
+constexpr int kHistBins = 66;  // k_tile_hist: tiles per nonzero count 0..64, then non-empty tile rows
+__global__ void k_tile_hist(const GraphDesc*, const Octile*, const int32_t*, int32_t*);
 
 // per-pair FP32 vectors of the panel slab / grid buffer (pcg_panel.cu)
 constexpr int kSlabVectors = 7;
@@ -176,5 +193,12 @@ cudaError_t launch_gram_normalize(double* K, int64_t G, double* diag, int* bad, 
 cudaError_t launch_pcg_block(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const PairJob& job,
                              const SolveParams& prm, const SolveOut& out, unsigned long long* queue,
                              float* scratch, int64_t scratch_floats_per_cta, int nctas, cudaStream_t stream);
+
+// Baseline orderings (order.cu): method MGK_REORDER_RCM or MGK_REORDER_MORTON; forward maps
+// (old -> new, local) of every graph; coords = the dataset's vector node labels (Morton).
+int order_device(int method, int G, const std::vector<GraphDesc>& graphs, const GraphDesc* d_graphs,
+                 const int32_t* d_node_graph, const int32_t* d_rowptr, const float4* d_rowent,
+                 const std::vector<double>& coords, int dim, cudaStream_t s, std::vector<int64_t>& forward,
+                 std::string& err);
 
 }  // namespace mgk

@@ -305,8 +305,9 @@ k_pcg_block(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     decode_pair(job, (int64_t)pid, ga, gb);
     const int64_t nm = (int64_t)ds.graphs[ga].n * ds.graphs[gb].n;
     // pairs at or below the tiny threshold run with FP64 vectors (CG there ends by Krylov exhaustion,
-    // which FP32 rounding delays; see pcg_warp.cu k_pcg_tiny), the rest with FP32 vectors
-    if (nm <= prm.tiny_nm)
+    // which FP32 rounding delays; see pcg_warp.cu k_pcg_tiny), and so does every pair of a precise
+    // kappa_e = 1 solve (kPreciseTol); the rest with FP32 vectors
+    if (nm <= prm.tiny_nm || prm.fp64)
       solve_block_pair<double>(ds, vk, ek, prm, out, scratch + (int64_t)blockIdx.x * slab, pid, ga, gb, red, &sh_carry);
     else
       solve_block_pair<float>(ds, vk, ek, prm, out, scratch + (int64_t)blockIdx.x * slab, pid, ga, gb, red, &sh_carry);

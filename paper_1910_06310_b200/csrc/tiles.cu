@@ -224,6 +224,22 @@ __global__ void k_trow(int G, const int64_t* __restrict__ gseg, const int64_t* _
   graphs[gidx] = g;
 }
 
+// Per-graph octile density histogram for the reference's cost counters (product.py:224-266): hist[g][k] =
+// tiles with k nonzeros (k = 1..64), hist[g][65] = non-empty tile rows.  One CTA per graph.
+__global__ void k_tile_hist(const GraphDesc* __restrict__ graphs, const Octile* __restrict__ tiles,
+                            const int32_t* __restrict__ trow, int32_t* __restrict__ hist) {
+  __shared__ int h[kHistBins];
+  const GraphDesc g = graphs[blockIdx.x];
+  for (int k = threadIdx.x; k < kHistBins; k += blockDim.x) h[k] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < g.ntiles; t += blockDim.x) atomicAdd(&h[__popcll(tiles[g.tile_off + t].bitmap)], 1);
+  const int32_t* tr = trow + g.trow_off;
+  for (int I = threadIdx.x; I < ceil8(g.n); I += blockDim.x)
+    if (tr[I + 1] > tr[I]) atomicAdd(&h[65], 1);
+  __syncthreads();
+  for (int k = threadIdx.x; k < kHistBins; k += blockDim.x) hist[(int64_t)blockIdx.x * kHistBins + k] = h[k];
+}
+
 // Row-ordered expansion of the octiles for the panel solver: node i's nonzeros
 // (ascending column, the order its tile row implies) land at
 // rowent[nz_off + rowptr[i] ..] as {col, w, label, log2 w}.  Thread per node.

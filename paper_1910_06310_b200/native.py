@@ -42,6 +42,7 @@ SIGNATURES = {
     "mgk_spatial_edges": (C.c_int, [C.c_int, C.c_int32, _P, C.c_int, _P, C.c_double, _P, _P, _P, _P, _P]),
     "mgk_bench_peaks": (C.c_int, [C.c_int, _P, _P]),
     "mgk_transfer_bytes": (C.c_int, [_P, _P]),
+    "mgk_counters": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _P, _P, C.c_int, _P]),
 }
 
 
@@ -133,10 +134,17 @@ class Context:
     def set_vertex_floor(self, v_min: float):
         check(self.lib.mgk_set_vertex_floor(self.h, float(v_min)))
 
-    def reorder_pbr(self, seed: int, apply: bool) -> np.ndarray:
+    REORDER = {"none": 0, "pbr": 1, "rcm": 2, "morton": 3}
+
+    def reorder(self, method: str, seed: int, apply: bool) -> np.ndarray:
+        """mgk_reorder: forward maps (old -> new, local per graph) of every graph, [sum n]."""
         out = np.empty(int(self.packed.node_off[-1]), dtype=np.int64)
-        check(self.lib.mgk_reorder(self.h, 1, C.c_uint64(seed & ((1 << 64) - 1)), int(apply), _ptr(out)))
+        check(self.lib.mgk_reorder(self.h, self.REORDER[method], C.c_uint64(seed & ((1 << 64) - 1)), int(apply),
+                                   _ptr(out)))
         return out
+
+    def reorder_pbr(self, seed: int, apply: bool) -> np.ndarray:
+        return self.reorder("pbr", seed, apply)
 
     def tiles(self, g: int):
         nt, nz = C.c_int32(), C.c_int32()
@@ -229,6 +237,15 @@ class Context:
         check(self.lib.mgk_pairs(self.h, k, _ptr(a), _ptr(b), float(tol), int(max_iter), _ptr(val), _ptr(it),
                                  _ptr(res), _ptr(cv), _ptr(nw)))
         return val, it, res, cv.astype(bool), nw
+
+    def counters(self, a: int, b: int, applies: int, model, thresholds, force_dense: bool) -> np.ndarray:
+        """mgk_counters: {flops, t1_load, t1_store, t2_load, t2_store, tile_pairs} after `applies` applies."""
+        m = np.array([model.E, model.F, model.X, model.r], dtype=np.float64)
+        th = np.array([thresholds.sparse_min_max, thresholds.sparse_max_max, thresholds.dense_min], dtype=np.int32)
+        out = np.empty(6, dtype=np.float64)
+        check(self.lib.mgk_counters(self.h, int(a), int(b), int(applies), _ptr(m), _ptr(th), int(bool(force_dense)),
+                                    _ptr(out)))
+        return out
 
     def peaks(self, device: int = 0):
         f, e = C.c_double(), C.c_double()

@@ -1,8 +1,10 @@
-"""Node reordering, mirroring ``mgksolver.reorder`` (reorder.py:29-404).
+"""Node reordering, mirroring ``mgksolver.reorder`` (reorder.py:29-478).
 
 ``pbr_reorder`` runs the device partition-based reordering (csrc/pbr.cu),
-bit-exact with the reference's recursive bisection + K-way FM refinement.
-``apply_permutation`` relabels a host graph (reorder.py:86-109).
+bit-exact with the reference's recursive bisection + K-way FM refinement;
+``rcm_reorder`` and ``morton_reorder`` run the device baselines (csrc/order.cu,
+bit-exact with reorder.py:412-478).  ``apply_permutation`` relabels a host
+graph (reorder.py:86-109).
 """
 
 from __future__ import annotations
@@ -85,3 +87,39 @@ def pbr_reorder(g: LabeledGraph, seed: int = 0, t: int = 8, max_passes: int = 10
     if t != 8 or max_passes != 10:
         raise NotImplementedError("device PBR is specialised to t=8, max_passes=10")
     return pbr_reorder_many([g], seed, device)[0]
+
+
+def _device_orders(graphs, method: str, seed: int = 0, device: int = 0) -> list[Permutation]:
+    from .solver import _ctx_lock, context
+
+    ctx = context(device)
+    pk = native.PackedDataset(graphs, with_labels=(method == "morton"))
+    with _ctx_lock:
+        ctx.upload(pk)
+        ctx.set_kernels(None, None)
+        fwd = ctx.reorder(method, seed, apply=False)
+    return [Permutation.from_forward(fwd[pk.node_off[k]: pk.node_off[k + 1]]) for k in range(len(graphs))]
+
+
+def rcm_reorder_many(graphs, device: int = 0) -> list[Permutation]:
+    """Device reverse Cuthill-McKee for a batch of graphs (one CTA per graph)."""
+    return _device_orders(graphs, "rcm", device=device)
+
+
+def rcm_reorder(g: LabeledGraph, device: int = 0) -> Permutation:
+    """reorder.py:412-443 on the device: components from their minimum-(degree, index) node, neighbours
+    by ascending (degree, index), each component reversed."""
+    return rcm_reorder_many([g], device)[0]
+
+
+def morton_reorder(points, device: int = 0) -> Permutation:
+    """reorder.py:471-478 on the device: Morton keys of 2-D / 3-D points (21 bits per axis over the
+    bounding box), sorted with ties by index."""
+    if points is None:
+        raise ValueError("Morton ordering requires node coordinates")
+    pts = np.asarray(points, dtype=np.float64)
+    if pts.ndim != 2 or pts.shape[1] not in (2, 3):
+        raise ValueError("points must be an (n, 2) or (n, 3) array")
+    g = LabeledGraph.from_arrays(len(pts), np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0),
+                                 node_labels=pts)
+    return _device_orders([g], "morton", device=device)[0]

@@ -18,6 +18,7 @@ import numpy as np
 from . import native
 from .basekernels import (as_kernel, BaseKernel, CompactPolynomial, ConstantOne, KroneckerDelta, ProductComposite,
                           RConvolution, SquareExponential)
+from .costs import CounterReport, SelectionThresholds, default_model
 from .graphs import LabeledGraph, validate_graph
 
 DEFAULT_VERTEX_FLOOR = 1e-12
@@ -86,7 +87,18 @@ def context(device: int = 0) -> native.Context:
         return ctx
 
 
-_REORDER_METHODS = ("pbr", "none", None)
+_REORDER_METHODS = ("pbr", "rcm", "morton", "none", None)
+# ProductOperator keywords (product.py:184-194).  Tiles, thresholds and cache limits only steer the
+# reference's plan (value-transparent, tests/test_product.py:297-316); cost_model, thresholds and
+# force_dense_stream shape the counters.
+_OPERATOR_OPTIONS = ("tiles_a", "tiles_b", "cost_model", "thresholds", "force_dense_stream", "cache_limit_bytes")
+
+
+def _edge_mode(g_a: LabeledGraph, g_b: LabeledGraph) -> str:
+    """product.py:153-161 (label-presence mismatch raises at upload, native.PackedDataset)."""
+    la = g_a.edge_labels is not None and g_a.edge_count > 0
+    lb = g_b.edge_labels is not None and g_b.edge_count > 0
+    return "labeled" if (la or lb) else "unlabeled"
 
 
 def kernel(g_a: LabeledGraph, g_b: LabeledGraph, vertex_kernel=None, edge_kernel=None,
@@ -98,12 +110,17 @@ def kernel(g_a: LabeledGraph, g_b: LabeledGraph, vertex_kernel=None, edge_kernel
         rep = validate_graph(g)
         if not rep.ok:
             raise ValueError(f"{name} graph invalid: " + "; ".join(rep.violations))
-    if reorder in ("rcm", "morton"):
-        raise NotImplementedError(f"{reorder} reordering is not on the device path (SURVEY.md §8f)")
     if reorder not in _REORDER_METHODS:
         raise ValueError(f"unknown reorder method {reorder!r}")
+    opts = dict(operator_options or {})
+    for key in opts:
+        if key not in _OPERATOR_OPTIONS:
+            raise TypeError(f"ProductOperator.__init__() got an unexpected keyword argument {key!r}")
     vk = as_kernel(vertex_kernel, "vertex")
     ek = as_kernel(edge_kernel, "edge")
+    mode = _edge_mode(g_a, g_b)
+    model = opts.get("cost_model") or default_model(g_a, g_b, mode, ek)
+    thresholds = opts.get("thresholds") or SelectionThresholds.for_mode(mode)
     start = time.perf_counter()
     ctx = context(device)
     with _ctx_lock:
@@ -111,14 +128,18 @@ def kernel(g_a: LabeledGraph, g_b: LabeledGraph, vertex_kernel=None, edge_kernel
         ctx.set_kernels(kernel_spec(vk), kernel_spec(ek))
         ctx.set_vertex_floor(cfg.v_min)
         perm = None
-        if reorder == "pbr":
-            perm = ctx.reorder_pbr(seed, apply=True)
+        if reorder and reorder != "none":  # same method and seed for both graphs (solver.py:236-237)
+            perm = ctx.reorder(reorder, seed, apply=True)
         val, it, res, cv, nw = ctx.pairs([0], [1], cfg.tolerance, cfg.max_iterations or 0, nodewise=True,
                                          sizes=[g_a.node_count, g_b.node_count])
+        # one operator apply per iteration (solver.py:98-99); counters of the (reordered) device octiles
+        cnt = ctx.counters(0, 1, int(it[0]), model, thresholds, bool(opts.get("force_dense_stream", False)))
     nodewise = nw.reshape(g_a.node_count, g_b.node_count)
     if perm is not None:
         fa, fb = perm[: g_a.node_count], perm[g_a.node_count:]
         nodewise = nodewise[fa[:, None], fb[None, :]]
+    counters = CounterReport(flops=float(cnt[0]), t1_load=float(cnt[1]), t1_store=float(cnt[2]),
+                             t2_load=float(cnt[3]), t2_store=float(cnt[4]), tile_pairs=int(cnt[5])).finalize()
     return KernelResult(value=float(val[0]), nodewise=nodewise, iterations=int(it[0]),
                         final_residual=float(res[0]), converged=bool(cv[0]),
-                        wall_time=time.perf_counter() - start)
+                        wall_time=time.perf_counter() - start, counters=counters)

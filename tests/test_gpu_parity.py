@@ -173,6 +173,16 @@ def test_gram_equals_pairs(mgk):
         for b in range(a, 12, 4):
             k = mgk.kernel(ds[a], ds[b], "delta:0.5", "se:1.0")
             assert res.matrix[a, b] == pytest.approx(k.value, rel=1e-6)
+    # mid graphs (25-40 nodes) against 1-5-node graphs: n m <= 128 pairs take the FP64 block solver in
+    # both entry points (one routing predicate), so the Gram and kernel() agree on values and iterations
+    rng = np.random.default_rng(4)
+    mix = [synth.molecule(rng, n) for n in (25, 31, 40)] + [synth.molecule(rng, n) for n in (1, 2, 4, 5)]
+    res = mgk.compute_gram(mix, "delta:0.5", "se:1.0")
+    for a in range(3):
+        for b in range(3, len(mix)):
+            k = mgk.kernel(mix[a], mix[b], "delta:0.5", "se:1.0")
+            assert res.matrix[a, b] == pytest.approx(k.value, rel=1e-12), (a, b)
+            assert res.iterations[a, b] == k.iterations
 
 
 def test_config2_sample_vs_oracle(mgk):
@@ -325,18 +335,11 @@ def test_dense_small_graph_tiny_pairs(mgk):
             o = O.solve_pcg(ga, gb, O.parse_spec(vs), O.parse_spec(es), tol=1e-10)
             assert abs(r.value - o.value) <= REL * abs(o.value)
             assert abs(r.iterations - o.iterations) <= 1, (vs, ga.node_count, gb.node_count, r.iterations, o.iterations)
-    # the Gram re-solves the same pairs on the FP64 block path (gram_fixup_job, capi.cu); K20 x K20
-    # (n m = 400) is not tiny and keeps the unlabeled FP32 protocol, so it is left out here
-    gs = [ds[0], ds[1], ds[4], k20]
-    res = mgk.compute_gram(gs, None, None, mgk.SolverConfig(tolerance=1e-10))
-    for a in range(4):
-        for b in range(a, 4):
-            if gs[a].node_count * gs[b].node_count > 128:
-                continue
-            o = O.solve_pcg(gs[a], gs[b], None, None, tol=1e-10)
-            assert abs(res.matrix[a, b] - o.value) <= REL * abs(o.value), (a, b)
-            assert abs(int(res.iterations[a, b]) - o.iterations) <= 1, (a, b, int(res.iterations[a, b]), o.iterations)
-    _check_gram_vs_oracle(mgk, [ds[0], ds[1], ds[4], k20, ds[2]])
+    # the Gram routes the same pairs to the FP64 block solver (the mid x small tiny job of gram_jobs);
+    # unlabeled at 1e-10 every pair runs there (kPreciseTol)
+    gs = [ds[0], ds[1], ds[4], k20, ds[2]]
+    for vs, es in [(None, None), (("delta", 0.5), ("se", 1.0))]:
+        _check_gram_vs_oracle(mgk, gs, vs, es, tol=1e-10)
 
 
 def test_medium_pairs_panel_kernel(mgk):
@@ -402,8 +405,11 @@ def test_gram_shards_cover_all_pairs(mgk):
     from paper_1910_06310_b200 import native, synth
 
     rng = np.random.default_rng(41)
+    ii, jj = np.triu_indices(20, 1)
+    k20 = mgk.LabeledGraph.from_arrays(20, ii, jj, rng.uniform(0.2, 2.0, ii.size), node_labels=rng.integers(0, 4, 20),
+                                       edge_labels=rng.uniform(0, 2, ii.size))
     ds = [synth.molecule(rng, int(n)) for n in rng.integers(4, 24, size=24)] + \
-         [synth.molecule(rng, int(n)) for n in (30, 45, 60)]
+         [synth.molecule(rng, int(n)) for n in (30, 45, 60, 2, 3)] + [k20]
     ctx = native.Context(0)
     ctx.upload(native.PackedDataset(ds))
     ctx.set_kernels("delta:0.5", "se:1.0")
@@ -426,7 +432,10 @@ def test_stream_nodewise_vs_oracle(mgk):
     from paper_1910_06310_b200 import synth
 
     rng = np.random.default_rng(21)
-    ds = [synth.molecule(rng, int(n)) for n in (5, 9, 14, 23, 30, 47)]
+    ii, jj = np.triu_indices(20, 1)
+    k20 = mgk.LabeledGraph.from_arrays(20, ii, jj, rng.uniform(0.2, 2.0, ii.size), node_labels=rng.integers(0, 4, 20),
+                                       edge_labels=rng.uniform(0, 2, ii.size))
+    ds = [synth.molecule(rng, int(n)) for n in (5, 9, 14, 23, 30, 47, 3)] + [k20]
     sizes = [g.node_count for g in ds]
     seen = {}
     chunks = []
@@ -441,7 +450,7 @@ def test_stream_nodewise_vs_oracle(mgk):
 
     for rank in range(2):
         mgk.stream_nodewise(ds, take, "delta:0.5", "se:1.0", chunk_bytes=4 * 1500, rank=rank, world=2)
-    assert sorted(seen) == [(a, b) for a in range(6) for b in range(a, 6)]
+    assert sorted(seen) == [(a, b) for a in range(8) for b in range(a, 8)]
     assert len(chunks) > 4
     for (a, b), (v, it, cv, field) in seen.items():
         o = O.solve_pcg(ds[a], ds[b], ("delta", 0.5), ("se", 1.0))

@@ -77,25 +77,32 @@ def _gram_vs_oracle(mgk, ds, vs, es, tol):
 
 
 @pytest.mark.parametrize("q", [5e-4, 5e-3])
-@pytest.mark.parametrize("path", ["default", "block", "grid"])
+@pytest.mark.parametrize("path", ["default", "block", "grid", "fp32"])
 def test_smallq_gram_every_class(mgk, monkeypatch, q, path):
     """Gram over tiny (FP64 warp), narrow / wide warp, panel, block (MGK_NO_PANEL) and grid (MGK_GRID_N
-    lowered) classes, unlabeled and kappa_e = 1 with a delta vertex kernel, at tol 1e-6 and 1e-8."""
+    lowered) classes, unlabeled and kappa_e = 1 with a delta vertex kernel, at tol 1e-6 and 1e-8.
+    By default these datasets take the precise FP64 block path (kPreciseTol / kPreciseLap); "fp32"
+    forces the FP32 solvers with the Laplacian splitting (MGK_FP64=0) at tol 1e-6."""
+    tols = (1e-6, 1e-8)
     if path == "block":
         monkeypatch.setenv("MGK_NO_PANEL", "1")
     if path == "grid":
         monkeypatch.setenv("MGK_GRID_N", "28")
+    if path == "fp32":
+        monkeypatch.setenv("MGK_FP64", "0")
+        tols = (1e-6,)
     for labeled, vs, es in ((False, None, None), (True, "delta:0.5", "const1")):
         ds = _smallq_dataset(mgk, q, labeled)
-        for tol in (1e-6, 1e-8):
+        for tol in tols:
             _gram_vs_oracle(mgk, ds, vs, es, tol)
 
 
 def test_smallq_splitting_is_needed(mgk, monkeypatch):
-    """The switch matters: with the splitting forced off (MGK_LAPLACIAN=0) an unlabeled q = 5e-4 pair
-    misses the 1e-5 bar, with it on (default) the same pair meets it."""
+    """The switch matters on the FP32 solvers: with the splitting forced off (MGK_LAPLACIAN=0) unlabeled
+    q = 5e-4 pairs lose accuracy, with it on (default) they meet the 1e-5 bar."""
     recs = [r for r in load_golden("smallq.json") if r["name"].startswith("u_q0.0005") and r["tol"] == 1e-8]
     errs = {}
+    monkeypatch.setenv("MGK_FP64", "0")  # the FP32 solvers (the precise FP64 path needs no splitting)
     for mode in ("0", "1"):
         monkeypatch.setenv("MGK_LAPLACIAN", mode)
         worst = 0.0
@@ -106,6 +113,19 @@ def test_smallq_splitting_is_needed(mgk, monkeypatch):
         errs[mode] = worst
     assert errs["1"] <= REL
     assert errs["0"] > errs["1"]
+
+
+@pytest.mark.parametrize("q", [0.05, 5e-4])
+def test_unlabeled_reference_default_tol(mgk, q):
+    """kappa_e = 1 solves below kPreciseTol (5e-7) run every pair with FP64 vectors on the block solver,
+    so unlabeled pairs meet +-1 iteration at the reference default tol 1e-10 (FP32 vectors need 3-8
+    more there: tools/precision_emulate.py), Gram and kernel() alike."""
+    ds = _smallq_dataset(mgk, q, False)
+    _gram_vs_oracle(mgk, ds, None, None, 1e-10)
+    for a, b in ((0, 10), (4, 5), (8, 9)):
+        r = mgk.kernel(ds[a], ds[b], None, None, mgk.SolverConfig(tolerance=1e-10))
+        o = O.solve_pcg(ds[a], ds[b], None, None, tol=1e-10)
+        assert abs(r.value - o.value) <= REL * abs(o.value) and abs(r.iterations - o.iterations) <= 1
 
 
 def test_laplacian_forced_on_normal_q(mgk, monkeypatch):

@@ -124,3 +124,30 @@ def test_synth_configs_shapes():
     c3 = synth.config3(count=2, n_lo=200, n_hi=210)
     assert all(200 <= g.node_count <= 210 for g in c3)
     assert synth.config2(count=5, seed=1)[3].edges_i.tolist() == synth.config2(count=5, seed=1)[3].edges_i.tolist()
+
+
+def test_predict_costs_golden():
+    """predict_costs (costs.py:74-128) against the reference's cells, exactly (counters.json)."""
+    from conftest import load_golden
+    from paper_1910_06310_b200 import CostModel, predict_costs
+
+    for rec in load_golden("counters.json")["predict"]:
+        got = predict_costs(CostModel(**rec["model"]), rec["n"], rec["m"], rec["primitive"])
+        for k, v in rec["report"].items():
+            assert getattr(got, k) == v, (rec["primitive"], rec["n"], rec["m"], k)
+
+
+def test_cost_model_validation_and_selection():
+    """costs.py:35-43 validation; product.py:56-66 selection with the reference's per-mode thresholds."""
+    from paper_1910_06310_b200 import CostModel, CounterReport, select_tile_kernel
+
+    for bad in ({"E": -1}, {"F": 0}, {"X": 0}, {"t": 8, "r": 3}):
+        with pytest.raises(ValueError):
+            CostModel(**bad)
+    assert select_tile_kernel(10, 16, "unlabeled") == "sparse-sparse"
+    assert select_tile_kernel(11, 16, "unlabeled") == "dense-sparse"
+    assert select_tile_kernel(16, 24, "labeled") == "sparse-sparse"
+    assert select_tile_kernel(32, 40, "labeled") == "dense-dense"
+    assert select_tile_kernel(5, 40, "labeled") == "dense-sparse"
+    rep = CounterReport(flops=100.0, t1_load=40.0, t1_store=10.0, t2_load=0.0, t2_store=0.0).finalize()
+    assert rep.ai1 == 2.0 and rep.ai2 is None

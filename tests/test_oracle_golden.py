@@ -6,7 +6,7 @@ these tests pin the oracle before it is trusted as the checker of the CUDA path.
 import numpy as np
 import pytest
 
-from conftest import graph_from_json
+from conftest import graph_from_json, load_golden
 from oracle import mgk_oracle as O
 
 
@@ -178,3 +178,27 @@ def test_spatial_edges_golden():
         ei, ej, w, d = O.spatial_edges(rec["points"], rec["cutoff"])
         assert ei.tolist() == rec["ei"] and ej.tolist() == rec["ej"]
         assert w.tolist() == rec["w"] and d.tolist() == rec["d"]
+
+
+def test_rcm_morton_oracle_golden():
+    """Oracle RCM / Morton restatements against the reference (order.json; the pbr_large.json graphs
+    carry the reference's rcm_reorder forward maps of 300-600-node proteins and RGGs)."""
+    order = load_golden("order.json")
+    for rec in order["rcm"]:
+        g = graph_from_json(rec["graph"])
+        assert O.rcm_order(g).tolist() == rec["forward"], rec["name"]
+    for rec in load_golden("pbr_large.json"):
+        assert O.rcm_order(graph_from_json(rec["graph"])).tolist() == rec["rcm"], rec["name"]
+    for rec in order["morton"]:
+        pts = np.asarray(rec["points"], dtype=np.float64)
+        assert O.morton_keys(pts).tolist() == rec["keys"], rec["name"]
+        assert O.morton_order(pts).tolist() == rec["forward"], rec["name"]
+
+
+def test_pbr_large_oracle_golden():
+    """Oracle PBR at config-3 sizes (300-600 nodes) against the reference's forward maps -- the two
+    smallest graphs (the oracle is pure Python; the GPU test covers all ten on the device)."""
+    recs = sorted(load_golden("pbr_large.json"), key=lambda r: r["graph"]["n"])[:2]
+    for rec in recs:
+        g = graph_from_json(rec["graph"])
+        assert O.pbr_reorder(g, seed=rec["seed"]).tolist() == rec["forward"], rec["name"]
