@@ -11,9 +11,10 @@ from .basekernels import (BaseKernel, CompactPolynomial, ConstantOne, KernelRang
                           KroneckerDelta, ProductComposite, RConvolution, SquareExponential, kernel_from_spec)
 from .costs import CostModel, CounterReport, PRIMITIVES, SelectionThresholds, predict_costs, select_tile_kernel
 from .graphs import DEFAULT_STOP_PROB, LabeledGraph, ValidationReport, validate_graph
-from .graphio import PointCloud, spatial_graph, spatial_graphs
+from .graphio import GraphFileError, PointCloud, load_edge_list, load_graph, save_graph, spatial_graph, spatial_graphs
 from .gram import (GramResult, compute_gram, load_gram_binary, load_gram_csv, nodewise_gram, normalize_gram,
-                   save_gram_binary, save_gram_csv, schedule_pairs, stream_nodewise)
+                   save_gram_binary, save_gram_csv, save_nodewise_csv, load_nodewise_csv, schedule_pairs,
+                   stream_nodewise)
 from .reorder import (Permutation, apply_permutation, morton_reorder, objective, partition_objective, pbr_reorder,
                       pbr_reorder_many, rcm_reorder, rcm_reorder_many)
 from .solver import KernelResult, SolverConfig, kernel

@@ -63,21 +63,36 @@ class TiledMatrix:
 
 
 def build_tiles(g: LabeledGraph, device: int = 0) -> TiledMatrix:
-    """Device octiles of one graph (tiles.py:85-127).  Values are the float32
-    copies the solver streams."""
+    """Device octiles of one graph (tiles.py:85-127) as the reference's host objects.
+
+    Rows, columns and bitmaps come from the device builder; each tile's payload
+    follows its bitmap in ascending bit order, as the reference stores it, with
+    the graph's float64 weights and its edge labels (the device streams float32
+    copies; the host view keeps the caller's values)."""
     from .solver import _ctx_lock, context
 
     ctx = context(device)
     with _ctx_lock:
         ctx.upload(native.PackedDataset([g], with_labels=False))
         ctx.set_kernels(None, None)
-        rc, bm, w = ctx.tiles(0)
-    tiles, off = [], 0
+        rc, bm, _ = ctx.tiles(0)
+    n = g.node_count
+    ei, ej = np.asarray(g.edges_i, dtype=np.int64), np.asarray(g.edges_j, dtype=np.int64)
+    # edge index of every (row, col) entry of the symmetric matrix, both directions
+    key = np.concatenate([ei * n + ej, ej * n + ei])
+    eid = np.concatenate([np.arange(len(ei)), np.arange(len(ei))])
+    order = np.argsort(key, kind="stable")
+    key, eid = key[order], eid[order]
+    w64 = np.asarray(g.weights, dtype=np.float64)
+    labels = None if g.edge_labels is None else np.asarray(g.edge_labels)
+    tiles = []
     for (r, c), b in zip(rc.tolist(), bm.tolist()):
-        k = bin(int(b)).count("1")
-        tiles.append(Tile(int(r), int(c), int(b), w[off: off + k].astype(np.float64)))
-        off += k
-    return TiledMatrix(g.node_count, TILE_SIZE, tiles)
+        b = int(b)
+        bits = np.array([k for k in range(64) if b >> k & 1], dtype=np.int64)
+        rows, cols = r * TILE_SIZE + bits // TILE_SIZE, c * TILE_SIZE + bits % TILE_SIZE
+        e = eid[np.searchsorted(key, rows * n + cols)]
+        tiles.append(Tile(int(r), int(c), b, w64[e], None if labels is None else labels[e]))
+    return TiledMatrix(n, TILE_SIZE, tiles)
 
 
 def dump_tiles(m: TiledMatrix) -> str:

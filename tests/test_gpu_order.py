@@ -122,3 +122,18 @@ def test_kernel_counters_reference_golden(mgk):
             assert r.counters.ai1 == ref["ai1"] and r.counters.ai2 == ref["ai2"], rec["name"]
     with pytest.raises(TypeError, match="unexpected keyword"):
         mgk.kernel(ga, gb, None, None, operator_options={"bogus": 1})
+
+
+def test_reference_graph_files_kernel(mgk):
+    """Graphs loaded from files the reference wrote give the reference's kernel value and nodewise CSV."""
+    import json
+
+    from conftest import GOLDEN
+
+    files = GOLDEN / "files"
+    index = json.loads((files / "index.json").read_text())
+    ga, gb = mgk.load_graph(files / "cat.json"), mgk.load_graph(files / "cat.json")
+    r = mgk.kernel(ga, gb, mgk.KroneckerDelta(0.5), mgk.SquareExponential(1.0))
+    assert abs(r.value - index["nodewise_value"]) <= 1e-5 * abs(index["nodewise_value"])
+    ref = mgk.load_nodewise_csv(files / "nodewise.csv")
+    assert np.max(np.abs(r.nodewise - ref)) <= 1e-5 * np.max(np.abs(ref))

@@ -45,9 +45,32 @@ def test_octiles_bit_exact(mgk, golden_structure):
 
 
 def test_build_tiles_api_dump(mgk, golden_structure):
+    """build_tiles host view: the reference's dump line, float64 values in (tile, bit) order equal to the
+    reference's, and per-nonzero edge labels through expand_tile (tiles.py:85-146)."""
     for rec in golden_structure[:6]:
-        t = mgk.build_tiles(graph_from_json(rec["graph"]))
+        g = graph_from_json(rec["graph"])
+        t = mgk.build_tiles(g)
         assert mgk.dump_tiles(t) == rec["tiles"]["dump"]
+        assert np.concatenate([x.weights for x in t.tiles]).tolist() == rec["tiles"]["values"], rec["name"]
+    rng = np.random.default_rng(130)
+    for edge_kind in ("cat", "vec"):
+        n = 21
+        iu, ju = np.triu_indices(n, 1)
+        keep = rng.random(iu.size) < 0.3
+        lab = rng.integers(0, 5, keep.sum()) if edge_kind == "cat" else rng.normal(size=(keep.sum(), 2))
+        g = mgk.LabeledGraph.from_arrays(n, iu[keep], ju[keep], rng.uniform(0.2, 2.0, keep.sum()), edge_labels=lab)
+        t, o = mgk.build_tiles(g), O.build_octiles(g)
+        assert [x.bitmap for x in t.tiles] == o.bitmaps
+        for k, tile in enumerate(t.tiles):
+            w, lb = mgk.expand_tile(tile)
+            sl = slice(o.offsets[k], o.offsets[k + 1])
+            assert np.array_equal(tile.weights, o.values[sl])
+            assert np.array_equal(tile.labels, o.labels[sl])
+            assert np.array_equal(w[tile.local_rows, tile.local_cols], o.values[sl])
+            if edge_kind == "cat":
+                holes = np.ones((8, 8), bool)
+                holes[tile.local_rows, tile.local_cols] = False
+                assert np.all(lb[holes] == -1)
 
 
 def _tol_for(rec):

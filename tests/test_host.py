@@ -151,3 +151,60 @@ def test_cost_model_validation_and_selection():
     assert select_tile_kernel(5, 40, "labeled") == "dense-sparse"
     rep = CounterReport(flops=100.0, t1_load=40.0, t1_store=10.0, t2_load=0.0, t2_store=0.0).finalize()
     assert rep.ai1 == 2.0 and rep.ai2 is None
+
+
+def _same_graph(g, rec):
+    ref = graph_from_json(rec)
+    assert g.node_count == ref.node_count
+    for f in ("edges_i", "edges_j", "weights", "start_prob", "stop_prob"):
+        assert np.array_equal(np.asarray(getattr(g, f)), np.asarray(getattr(ref, f))), f
+    for f in ("node_labels", "edge_labels"):
+        a, b = getattr(g, f), getattr(ref, f)
+        assert (a is None) == (b is None), f
+        if a is not None:
+            assert np.array_equal(np.asarray(a).reshape(len(a), -1), np.asarray(b).reshape(len(b), -1)), f
+
+
+def test_graph_files_reference_fixtures(tmp_path):
+    """load_graph / load_edge_list on files the reference wrote (graphio.py:61-208), save -> load round
+    trip, and the reference's GraphFileError texts."""
+    import json
+
+    from conftest import GOLDEN
+    from paper_1910_06310_b200 import GraphFileError, load_edge_list, load_graph, save_graph
+
+    files = GOLDEN / "files"
+    index = json.loads((files / "index.json").read_text())
+    for name in ("cat", "vec", "plain"):
+        g = load_graph(files / f"{name}.json")
+        _same_graph(g, index[name])
+        save_graph(g, tmp_path / f"{name}.json")
+        assert json.loads((tmp_path / f"{name}.json").read_text()) == json.loads((files / f"{name}.json").read_text())
+    _same_graph(load_edge_list(files / "edges.txt"), index["edges"])
+    bad = {"missing": ({"node_count": 2, "nodes": []}, "missing field 'edges'"),
+           "count": ({"node_count": 2, "nodes": [{"id": 0}], "edges": []}, "nodes: expected 2 entries, got 1"),
+           "ids": ({"node_count": 2, "nodes": [{"id": 0}, {"id": 2}], "edges": []}, "ids must be dense 0..1"),
+           "kind": ({"node_count": 1, "nodes": [{"id": 0}], "edges": [], "node_label_kind": "x"}, "unknown label kind"),
+           "edge": ({"node_count": 2, "nodes": [{"id": 0}, {"id": 1}], "edges": [{"i": 0, "j": 5, "w": 1.0}]},
+                    "edge 0: unknown node id 5"),
+           "label": ({"node_count": 2, "nodes": [{"id": 0}, {"id": 1}], "edges": [{"i": 0, "j": 1, "w": 1, "label": 2}]},
+                     "edge 0: label present but kind is none")}
+    for key, (doc, msg) in bad.items():
+        (tmp_path / f"{key}.json").write_text(json.dumps(doc))
+        with pytest.raises(GraphFileError, match=msg):
+            load_graph(tmp_path / f"{key}.json")
+    (tmp_path / "e.txt").write_text("0 1 2 3\n")
+    with pytest.raises(GraphFileError, match="line 1: expected 'i j \\[w\\]'"):
+        load_edge_list(tmp_path / "e.txt")
+
+
+def test_nodewise_csv_roundtrip(tmp_path):
+    """save_nodewise_csv writes the CLI's nodewise format (cli.py:65-69): reading the reference's file
+    back and writing it again reproduces it byte for byte."""
+    from conftest import GOLDEN
+    from paper_1910_06310_b200 import load_nodewise_csv, save_nodewise_csv
+
+    src = GOLDEN / "files" / "nodewise.csv"
+    field = load_nodewise_csv(src)
+    save_nodewise_csv(field, tmp_path / "nw.csv")
+    assert (tmp_path / "nw.csv").read_text() == src.read_text()
