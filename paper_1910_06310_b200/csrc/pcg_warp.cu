@@ -118,21 +118,130 @@ __device__ __forceinline__ double shifted_diag(const DatasetDev& ds, double diag
 // Tiny product systems (n*m <= prm.tiny_nm, default 128): CG terminates there
 // by Krylov exhaustion, which FP32 rounding in the matvec delays by a few
 // iterations.  These pairs run the same algorithm with FP64 vectors and FP64
-// accumulation (coefficients stay FP32), which restores the reference's
-// iteration counts; element e of the field is owned by lane e % 32.
+// accumulation (edge-kernel coefficients stay FP32), which restores the
+// reference's iteration counts.
+//
+// The matvec uses the warp solver's lane-slot mapping: the warp walks the
+// rows of U (the graph with more nonzeros) in lock step, lane l owns the
+// nonzeros l + 32 t of L (t < NS <= 4: min(n, m) <= 11 gives S_L <= 110), so
+// every lane runs the same trip counts -- no divergent per-element loops.
+// The field lives compactly as [i * m + l] (a warp-uniform row j gathers
+// P[j * m + col_L(t)], consecutive banks); the vector phase gives lane e % 32
+// the elements e (<= 4 per lane).
 // ---------------------------------------------------------------------------
 constexpr int kTinyMax = 128;
+constexpr int kTinySlots = 4;
+
+struct TinySmem {
+  double P[kTinyMax];
+  double AP[kTinyMax];
+  double DG[kTinyMax];
+  double SS[kTinyMax];
+  double SEG[2 * 32 * kTinySlots];  // slot products of two U rows, segment-summed per L row
+  float4 UE[SMAX];                  // U nonzeros: {weight form, label, P row offset j * m, -}
+  int urow[NU + 8];
+  int lrow[40];
+};
+
+// AP = SS * P - OFF for all U rows; OFF[i][l] = sum_{k in U(i)} sum_{t in L(l)} kappa w_k w'_t P[j_k][col_t]
+// (Laplacian splitting: P[j_k][col_t] - P[i][l] instead of P[j_k][col_t]).
+template <int NS, int EK, bool LAP>
+__device__ __forceinline__ void tiny_xmv(TinySmem& S, const KernelDesc& ek, int nu, int m, int lane,
+                                         const int (&lcol)[kTinySlots], const int (&lrw)[kTinySlots],
+                                         const float (&lw)[kTinySlots], const float (&llab)[kTinySlots], int lr0,
+                                         int lr1) {
+  for (int i = 0; i < nu; i += 2) {
+    const bool two = i + 1 < nu;
+    double acc[2][NS];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int t = 0; t < NS; ++t) acc[r][t] = 0.0;
+      if (r == 1 && !two) break;
+      const int row = i + r;
+      double pc[NS];
+#pragma unroll
+      for (int t = 0; t < NS; ++t) pc[t] = LAP ? S.P[row * m + lrw[t]] : 0.0;
+      for (int k = S.urow[row]; k < S.urow[row + 1]; ++k) {
+        const float4 e = S.UE[k];
+        const double* pr = S.P + __float_as_int(e.z);
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+          const double pv = LAP ? pr[lcol[t]] - pc[t] : pr[lcol[t]];
+          acc[r][t] = fma((double)edge_kappa_w<EK>(ek, e.y, llab[t], e.x), pv, acc[r][t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      S.SEG[lane + 32 * t] = acc[0][t] * (double)lw[t];
+      S.SEG[32 * NS + lane + 32 * t] = acc[1][t] * (double)lw[t];
+    }
+    __syncwarp();
+    if (lane < m) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int q = lr0; q < lr1; ++q) {
+        s0 += S.SEG[q];
+        s1 += S.SEG[32 * NS + q];
+      }
+      const int e0 = i * m + lane;
+      S.AP[e0] = S.SS[e0] * S.P[e0] - s0;
+      if (two) S.AP[e0 + m] = S.SS[e0 + m] * S.P[e0 + m] - s1;
+    }
+    __syncwarp();
+  }
+}
+
+template <int EK, bool LAP>
+__device__ __forceinline__ void tiny_xmv_dispatch(int ns, TinySmem& S, const KernelDesc& ek, int nu, int m,
+                                                  int lane, const int (&lcol)[kTinySlots],
+                                                  const int (&lrw)[kTinySlots], const float (&lw)[kTinySlots],
+                                                  const float (&llab)[kTinySlots], int lr0, int lr1) {
+  switch (ns) {
+    case 1: tiny_xmv<1, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
+    case 2: tiny_xmv<2, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
+    case 3: tiny_xmv<3, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
+    case 4: tiny_xmv<4, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
+    default:  // edgeless L: OFF = 0 (an edgeless U has no rows to walk either)
+      for (int e = lane; e < nu * m; e += 32) S.AP[e] = S.SS[e] * S.P[e];
+      __syncwarp();
+  }
+}
 
 template <int EK>
-__device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek, const SolveParams& prm,
-                           const SolveOut& out, const GraphDesc& U, const GraphDesc& L, const float2* uwl,
-                           const int* uoff, const int* urow, const float4* le, const int* lrow, double* P, double* AP,
-                           double* DG, double* SS, int lane, double& value_out, int64_t& it_out, bool& conv_out,
-                           double& rr_out, float* nw, bool swap) {
+__device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& vk, const KernelDesc& ek,
+                                        const SolveParams& prm, const SolveOut& out, const GraphDesc& U,
+                                        const GraphDesc& L, TinySmem& S, int lane, double& value_out, int64_t& it_out,
+                                        bool& conv_out, double& rr_out, float* nw, bool swap) {
   const int nu = U.n, m = L.n, nm = nu * m;
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
   // kappa_e = 1 with a large diag / s: A p = s p - sum c (p_j - p_i), s in FP64 (mgk_dev.cuh kLapFactor)
   const bool lap = EK == KK_NONE && laplacian_pair(prm, U, L);
+  // lane slots of L: nonzero k' = lane + 32 t -> column, row, weight, label
+  const int SL = 2 * L.ne, ns = (SL + 31) >> 5;
+  int lcol[kTinySlots], lrw[kTinySlots];
+  float lw[kTinySlots], llab[kTinySlots];
+  {
+    const float4* lr = ds.rowent + L.nz_off;
+#pragma unroll
+    for (int t = 0; t < kTinySlots; ++t) {
+      const int k = lane + 32 * t;
+      lcol[t] = 0;
+      lrw[t] = 0;
+      lw[t] = 0.0f;
+      llab[t] = 0.0f;
+      if (k < SL) {
+        const float4 e = lr[k];
+        lcol[t] = __float_as_int(e.x);
+        lw[t] = e.y;
+        llab[t] = e.z;
+        int r = 0;
+        while (S.lrow[r + 1] <= k) ++r;
+        lrw[t] = r;
+      }
+    }
+  }
+  const int lr0 = lane < m ? S.lrow[lane] : 0, lr1 = lane < m ? S.lrow[lane + 1] : 0;
   double r[4], x[4];
   double bb_u = 0.0, bb_l = 0.0;
   if (lane < nu) {
@@ -154,11 +263,11 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
       const int64_t vu = U.node_off + i, vl = L.node_off + l;
       const double dg = diag_of(ds, vk, prm, out, vlab, vu, vl);
       const double b = (ds.deg[vu] * ds.q64[vu]) * (ds.deg[vl] * ds.q64[vl]);
-      DG[e] = dg;
-      SS[e] = lap ? shifted_diag(ds, dg, vu, vl) : dg;
+      S.DG[e] = dg;
+      S.SS[e] = lap ? shifted_diag(ds, dg, vu, vl) : dg;
       r[s] = b;
       const double z = b / dg;
-      P[e] = z;
+      S.P[e] = z;
       rho += b * z;
       rr += b * b;
     }
@@ -171,32 +280,16 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
   int64_t it = 0;
   __syncwarp();
   while (!conv && it < max_iter) {
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int e = lane + 32 * s;
-      if (e < nm) {
-        const int i = e / m, l = e - i * m;
-        const double pc = lap ? P[e] : 0.0;
-        double acc = 0.0;
-        for (int k = urow[i]; k < urow[i + 1]; ++k) {
-          const float2 a = uwl[k];
-          const double* prow = P + (uoff[k] >> 7) * m;
-          for (int q = lrow[l]; q < lrow[l + 1]; ++q) {
-            const float4 b = le[q];
-            const float c = edge_kappa<EK>(ek, a.y, b.z) * a.x * b.y;
-            acc = fma((double)c, prow[__float_as_int(b.x)] - pc, acc);
-          }
-        }
-        AP[e] = SS[e] * P[e] - acc;
-      }
-    }
-    __syncwarp();
+    if (lap)
+      tiny_xmv_dispatch<EK, true>(ns, S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1);
+    else
+      tiny_xmv_dispatch<EK, false>(ns, S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1);
     ++it;
     double pap = 0.0;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
-      if (e < nm) pap += P[e] * AP[e];
+      if (e < nm) pap += S.P[e] * S.AP[e];
     }
     const double alpha = rho / warp_sum(pap);
     double rr_l = 0.0, rz_l = 0.0;
@@ -204,10 +297,10 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
       if (e < nm) {
-        x[s] += alpha * P[e];
-        r[s] -= alpha * AP[e];
+        x[s] += alpha * S.P[e];
+        r[s] -= alpha * S.AP[e];
         rr_l += r[s] * r[s];
-        rz_l += r[s] * (r[s] / DG[e]);
+        rz_l += r[s] * (r[s] / S.DG[e]);
       }
     }
     rr = warp_sum(rr_l);
@@ -221,7 +314,7 @@ __device__ __noinline__ void solve_tiny(const DatasetDev& ds, const KernelDesc& 
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
-      if (e < nm) P[e] = r[s] / DG[e] + beta * P[e];
+      if (e < nm) S.P[e] = r[s] / S.DG[e] + beta * S.P[e];
     }
     rho = rho_next;
     __syncwarp();
@@ -630,15 +723,6 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
 }
 
 // Tiny-pair kernel: warp per pair, FP64 vectors (see solve_tiny).
-struct TinySmem {
-  float2 UWL[SMAX];
-  int UOFF[SMAX];
-  float4 LE[SMAX];
-  double V[4 * kTinyMax];  // P, AP, DG, SS
-  int urow[NU + 8];
-  int lrow[40];
-};
-
 template <int EK>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
@@ -646,7 +730,6 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   TinySmem& S = reinterpret_cast<TinySmem*>(smem_raw)[threadIdx.x >> 5];
-  const int el_dim = ds.el_dim;
   for (;;) {
     unsigned long long pid = 0;
     if (lane == 0) pid = atomicAdd(queue, 1ull);
@@ -655,26 +738,25 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int32_t ga, gb;
     decode_pair(job, (int64_t)pid, ga, gb);
     const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
+    // U = the graph with more nonzeros (rows walked by the warp), L = the other (lane slots); the
+    // smaller node count bounds S_L <= 110 <= 32 * kTinySlots
+    const bool swap = (2 * B.ne > 2 * A.ne) || (B.ne == A.ne && B.n > A.n);
+    const GraphDesc U = swap ? B : A, L = swap ? A : B;
     {  // rows from the dataset's row expansion of the octiles (see k_pcg_warp)
-      const float4* ar = ds.rowent + A.nz_off;
-      const float4* br = ds.rowent + B.nz_off;
-      for (int k = lane; k < 2 * A.ne; k += 32) {
-        const float4 e = ar[k];
-        S.UWL[k] = make_float2(e.y, e.z);
-        S.UOFF[k] = __float_as_int(e.x) * 128;
+      const float4* ur = ds.rowent + U.nz_off;
+      for (int k = lane; k < 2 * U.ne; k += 32) {
+        const float4 e = ur[k];
+        S.UE[k] = make_float4(EK == KK_SE ? e.w : e.y, e.z, __int_as_float(__float_as_int(e.x) * L.n), 0.0f);
       }
-      for (int k = lane; k < 2 * B.ne; k += 32) S.LE[k] = br[k];
-      if (lane <= A.n) S.urow[lane] = ds.rowptr[A.rowptr_off + lane];
-      if (lane <= B.n) S.lrow[lane] = ds.rowptr[B.rowptr_off + lane];
+      if (lane <= U.n) S.urow[lane] = ds.rowptr[U.rowptr_off + lane];
+      if (lane <= L.n) S.lrow[lane] = ds.rowptr[L.rowptr_off + lane];
     }
-    (void)el_dim;
     __syncwarp();
     double val, rr;
     int64_t it;
     bool conv;
     float* nw = out.nodewise ? out.nodewise + out.nodewise_off[pid] : nullptr;
-    solve_tiny<EK>(ds, vk, ek, prm, out, A, B, S.UWL, S.UOFF, S.urow, S.LE, S.lrow, S.V, S.V + kTinyMax,
-                   S.V + 2 * kTinyMax, S.V + 3 * kTinyMax, lane, val, it, conv, rr, nw, false);
+    solve_tiny<EK>(ds, vk, ek, prm, out, U, L, S, lane, val, it, conv, rr, nw, swap);
     write_pair_outputs(out, pid, ga, gb, val, it, conv, rr, lane);
     __syncwarp();
   }
