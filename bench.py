@@ -303,46 +303,57 @@ def run_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
 
+    gram_out = {}
+
+    bucket_ms = [[] for _ in bks]
+
     def step():
         """One Gram per bucket (N=1: device-resident result; N>1: shard + gather to rank 0)."""
         ms_tot, nl_tot, g_tot = 0.0, 0, 0.0
-        for ctx, (_, ds) in zip(ctxs, bks):
+        for bi, (ctx, (_, ds)) in enumerate(zip(ctxs, bks)):
+            ms_before = ms_tot
             if cfg.nodewise:
                 ctx.gram_nodewise(rank, world, cfg.tol, _discard, NW_CHUNK)
                 ms, launches = ctx.last_timing()
                 ms_tot += ms
                 nl_tot += launches
+                bucket_ms[bi].append(ms)
                 continue
             if world == 1:
                 ctx.gram(cfg.tol, fetch=False)
                 ms, launches = ctx.last_timing()
                 ms_tot += ms
                 nl_tot += launches
+                bucket_ms[bi].append(ms)
                 continue
-            pa, pb, v, it, cv = ctx.gram_shard(rank, world, cfg.tol)
+            # shard records straight into device tensors (mgk_gram_shard_device), NCCL gather of the
+            # padded records to rank 0, device-side assembly of the mirrored matrix (mgk_gram_assemble)
+            n = ctx.gram_shard_device(rank, world, cfg.tol)
+            nmax = torch.tensor([n], device=dev)
+            dist.all_reduce(nmax, op=dist.ReduceOp.MAX)
+            cap = int(nmax.item())
+            rec = [torch.full((cap,), -1, dtype=torch.int32, device=dev), torch.full((cap,), -1, dtype=torch.int32,
+                   device=dev), torch.empty(cap, dtype=torch.float64, device=dev),
+                   torch.empty(cap, dtype=torch.int32, device=dev), torch.zeros(cap, dtype=torch.uint8, device=dev)]
+            ctx.gram_shard_device(rank, world, cfg.tol, out=rec)
             ms, launches = ctx.last_timing()
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record()
-            payload = torch.from_numpy(np.stack([pa.astype(np.float64), pb.astype(np.float64), v,
-                                                 it.astype(np.float64) + 0.5 * cv]).T.copy()).to(dev)
-            n = torch.tensor([payload.shape[0]], device=dev)
-            nmax = n.clone()
-            dist.all_reduce(nmax, op=dist.ReduceOp.MAX)
-            pad = torch.zeros((int(nmax.item()), 4), dtype=torch.float64, device=dev)
-            pad[: payload.shape[0]] = payload
-            pad[payload.shape[0]:, 0] = -1
-            out = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
-            dist.gather(pad, out, dst=0)
+            outs = gather_records(rec, rank, world, dist)
+            if rank == 0:
+                G = len(ds)
+                if gram_out.get(G) is None:
+                    gram_out[G] = (torch.empty((G, G), dtype=torch.float64, device=dev),
+                                   torch.empty((G, G), dtype=torch.int32, device=dev),
+                                   torch.empty((G, G), dtype=torch.uint8, device=dev))
+                native.gram_assemble(local_rank, outs, G, *gram_out[G])
             t1.record()
             torch.cuda.synchronize(dev)
-            if rank == 0:
-                allp = torch.cat(out).cpu().numpy()
-                allp = allp[allp[:, 0] >= 0]
-                assemble(allp, len(ds))
             ms_tot += ms
-            nl_tot += launches
+            nl_tot += launches + (1 if rank == 0 else 0)
             g_tot += t0.elapsed_time(t1)
+            bucket_ms[bi].append(ms)
         return ms_tot, nl_tot, g_tot
 
     for w in range(args.warmup):
@@ -376,7 +387,9 @@ def run_ours(args, rank, world, local_rank):
 
         flops = exps = dense = 0.0
         Ks = []
-        for ctx, (_, ds) in zip(ctxs, bks):
+        fp32_peak, ex2_peak = ctxs[0].peaks(local_rank)
+        per_bucket = []
+        for bi, (ctx, (bname, ds)) in enumerate(zip(ctxs, bks)):
             K, it, cv = ctx.gram(cfg.tol)
             Ks.append((K, it))
             G = len(ds)
@@ -384,10 +397,23 @@ def run_ours(args, rank, world, local_rank):
             S = 2.0 * np.array([g.edge_count for g in ds], dtype=np.float64)
             iu, ju = np.triu_indices(G)
             iters = it[iu, ju].astype(np.float64)
-            flops += float(np.sum(iters * (cfg.x_flops * S[iu] * S[ju] + 15.0 * n[iu] * n[ju])))
+            f_b = float(np.sum(iters * (cfg.x_flops * S[iu] * S[ju] + 15.0 * n[iu] * n[ju])))
+            flops += f_b
             T = np.array([octile_count(g) for g in ds], dtype=np.float64)
-            dense += float(np.sum(iters * cfg.x_flops * 4096.0 * T[iu] * T[ju]))
+            d_b = float(np.sum(iters * cfg.x_flops * 4096.0 * T[iu] * T[ju]))
+            dense += d_b
             exps += float(np.sum(iters * S[iu] * S[ju])) if cfg.espec == "se:1.0" else 0.0
+            if len(bks) > 1:  # per-density-bucket evidence (BASELINE configs[3])
+                ms_b = float(np.mean(bucket_ms[bi]))
+                per_bucket.append({
+                    "bucket": bname, "graphs": G, "pairs": G * (G + 1) // 2, "ms": ms_b,
+                    "pairs_per_s": G * (G + 1) / 2 / (ms_b * 1e-3),
+                    "mean_tile_nnz": float(S.sum() / T.sum()) if T.sum() else 0.0,
+                    "mean_iterations": float(iters.mean()),
+                    "eff_tflops": f_b / (ms_b * 1e-3) / 1e12,
+                    "fp32_frac": f_b / (ms_b * 1e-3) / 1e12 / fp32_peak,
+                    "dense_tile_tflops": d_b / (ms_b * 1e-3) / 1e12,
+                })
             del iu, ju
         worst, it_dev, checked = 0.0, 0, 0
         if cfg.parity_pairs:
@@ -402,7 +428,6 @@ def run_ours(args, rank, world, local_rank):
                 checked += 1
         del Ks
         log(f"parity sample done ({checked} pairs)")
-        fp32_peak, ex2_peak = ctxs[0].peaks(local_rank)
         achieved = flops / world / (ms_solve * 1e-3) / 1e12
         traffic, traffic_src = traffic_from_profiles(cfg)
 
@@ -505,6 +530,8 @@ def run_ours(args, rank, world, local_rank):
                        "bar": "1e-5 relative, +-1 iteration"},
             "solve_ms_per_step": ms_solve,
         }
+        if per_bucket:
+            result["buckets"] = per_bucket
         if cfg.reorder:
             result["preprocess_s"] = {"device_pbr_and_apply": reorder_s}
     if dist is not None:
@@ -541,16 +568,33 @@ def _solver_cfg(cfg: Config):
     return SolverConfig(tolerance=cfg.tol)
 
 
-def assemble(rows: np.ndarray, G: int):
-    """Scatter gathered (a, b, value, iters + conv/2) rows into the mirrored Gram matrix."""
-    a = rows[:, 0].astype(np.int64)
-    b = rows[:, 1].astype(np.int64)
-    conv = (rows[:, 3] % 1.0) > 0.25
-    v = np.where(conv, rows[:, 2], np.nan)
+def gather_records(rec, rank: int, world: int, dist):
+    """Gather every rank's padded shard records (pair_a, pair_b, value, iterations, converged; equal
+    lengths, graph id -1 = padding) to rank 0: one collective per field (NCCL on device tensors in the
+    bench, gloo on CPU tensors in tests/test_dist_gloo.py).  Returns the concatenated fields on rank 0,
+    None elsewhere."""
+    import torch
+
+    outs = []
+    for t in rec:
+        o = [torch.empty_like(t) for _ in range(world)] if rank == 0 else None
+        dist.gather(t, o, dst=0)
+        outs.append(torch.cat(o) if rank == 0 else None)
+    return outs if rank == 0 else None
+
+
+def assemble_host(recs, G: int):
+    """Host statement of mgk_gram_assemble (gram_post.cu) for the CPU multi-rank test: mirrored writes,
+    NaN where not converged, padding skipped."""
+    a, b, v, it, cv = [np.asarray(t) for t in recs]
+    keep = a >= 0
+    a, b, v, it, cv = a[keep].astype(np.int64), b[keep].astype(np.int64), v[keep], it[keep], cv[keep].astype(bool)
     K = np.zeros((G, G))
-    K[a, b] = v
-    K[b, a] = v
-    return K
+    I = np.zeros((G, G), dtype=np.int32)
+    vv = np.where(cv, v, np.nan)
+    K[a, b] = K[b, a] = vv
+    I[a, b] = I[b, a] = it
+    return K, I
 
 
 # ---------------------------------------------------------------------------

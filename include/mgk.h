@@ -116,6 +116,32 @@ int mgk_gram_normalized(mgk_ctx* ctx, double tol, int64_t max_iter, double* K, i
 int mgk_gram_shard(mgk_ctx* ctx, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
                    int32_t* pair_a, int32_t* pair_b, double* value, int32_t* iters, uint8_t* conv);
 
+/* mgk_gram_shard with the per-pair records written to caller-owned DEVICE
+ * buffers on this context's device (no host round trip): the input of a
+ * device-side gather (NCCL / peer copies) in multi-process runs.  All outputs
+ * NULL: only *npairs_out. */
+int mgk_gram_shard_device(mgk_ctx* ctx, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
+                          int32_t* d_pair_a, int32_t* d_pair_b, double* d_value, int32_t* d_iters,
+                          uint8_t* d_conv);
+
+/* Assemble gathered shard records (device buffers on `device`, graph ids < 0
+ * mark padding) into device-resident G x G matrices: mirrored writes, NaN
+ * where the pair did not converge (gram.py:86-90).  Any matrix may be NULL. */
+int mgk_gram_assemble(int device, int64_t npairs, const int32_t* d_pair_a, const int32_t* d_pair_b,
+                      const double* d_value, const int32_t* d_iters, const uint8_t* d_conv, int64_t G, double* d_K,
+                      int32_t* d_K_iters, uint8_t* d_K_conv);
+
+/* All-pairs Gram over several devices from ONE host process (north_star (4):
+ * the N(N+1)/2 pair list load-balanced over the GPUs of a box, no collective
+ * beyond the final gather; the reference's pair queue, gram.py:69-86).  Every
+ * context holds the same dataset and kernels (one context per device);
+ * context k solves the cost-ordered pair ids congruent to k mod nctx on its own
+ * host thread and scatters its compact results straight into the caller's
+ * K / iters / conv (mirrored, NaN where not converged).  mgk_last_timing of
+ * each context then reports the slowest device's solve time. */
+int mgk_gram_multi(mgk_ctx* const* ctxs, int nctx, double tol, int64_t max_iter, double* K, int32_t* iters,
+                   uint8_t* conv);
+
 /* Batch of explicit pairs (the per-pair `kernel` of solver.py:212-246 without
  * reordering): value[k], iters[k], residual[k], conv[k]; nodewise (nullable)
  * receives the n_a x m_b float64 field of every pair back to back. */

@@ -1,6 +1,7 @@
 // libmgk C-ABI: context, dataset upload/validation, label lowering, device
 // preprocessing (octiles, degrees, PBR) and solver dispatch.  See include/mgk.h.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -9,6 +10,8 @@
 #include <map>
 #include <numeric>
 #include <set>
+#include <thread>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -22,7 +25,7 @@ namespace {
 
 thread_local std::string g_err;
 // cumulative host<->device payload bytes (benchmark accounting)
-int64_t g_h2d_bytes = 0, g_d2h_bytes = 0;
+std::atomic<int64_t> g_h2d_bytes{0}, g_d2h_bytes{0};
 
 cudaError_t d2h(void* dst, const void* src, size_t bytes) {
   g_d2h_bytes += (int64_t)bytes;
@@ -1157,8 +1160,10 @@ static int64_t shard_len(int64_t total, int rank, int world) {
   return total > rank ? (total - rank + world - 1) / world : 0;
 }
 
-int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
-                   int32_t* pair_a, int32_t* pair_b, double* value, int32_t* iters, uint8_t* conv) {
+// Shard jobs of the Gram (pair ids congruent to rank mod world of every class job) solved into the
+// per-pair device outputs `o` (null: count only).
+static int gram_shard_run(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
+                          SolveOut* o) {
   if (!c) return fail(MGK_E_INVALID, "null context");
   if (world < 1 || rank < 0 || rank >= world) return fail(MGK_E_INVALID, "bad rank/world");
   if (!(tol > 0)) return fail(MGK_E_INVALID, "tolerance must be positive");
@@ -1179,6 +1184,16 @@ int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter
     total += len;
   }
   if (npairs_out) *npairs_out = total;
+  if (!o) return MGK_OK;
+  return run_jobs(c, jobs, *o, offs, prm);
+}
+
+int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
+                   int32_t* pair_a, int32_t* pair_b, double* value, int32_t* iters, uint8_t* conv) {
+  int64_t total = 0;
+  int rc = gram_shard_run(c, rank, world, tol, max_iter, &total, nullptr);
+  if (rc) return rc;
+  if (npairs_out) *npairs_out = total;
   if (!pair_a && !pair_b && !value && !iters && !conv) return MGK_OK;
   CUDA_TRY(c->d_value.alloc(total));
   CUDA_TRY(c->d_iters.alloc(total));
@@ -1191,13 +1206,109 @@ int mgk_gram_shard(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter
   o.conv = c->d_conv.ptr;
   o.pair_a = c->d_pa.ptr;
   o.pair_b = c->d_pb.ptr;
-  rc = run_jobs(c, jobs, o, offs, prm);
+  rc = gram_shard_run(c, rank, world, tol, max_iter, nullptr, &o);
   if (rc) return rc;
   if (pair_a) CUDA_TRY(d2h(pair_a, c->d_pa.ptr, total * sizeof(int32_t)));
   if (pair_b) CUDA_TRY(d2h(pair_b, c->d_pb.ptr, total * sizeof(int32_t)));
   if (value) CUDA_TRY(d2h(value, c->d_value.ptr, total * sizeof(double)));
   if (iters) CUDA_TRY(d2h(iters, c->d_iters.ptr, total * sizeof(int32_t)));
   if (conv) CUDA_TRY(d2h(conv, c->d_conv.ptr, total));
+  return MGK_OK;
+}
+
+int mgk_gram_shard_device(mgk_ctx* c, int rank, int world, double tol, int64_t max_iter, int64_t* npairs_out,
+                          int32_t* d_pair_a, int32_t* d_pair_b, double* d_value, int32_t* d_iters, uint8_t* d_conv) {
+  if (!d_pair_a && !d_pair_b && !d_value && !d_iters && !d_conv)
+    return gram_shard_run(c, rank, world, tol, max_iter, npairs_out, nullptr);
+  SolveOut o{};
+  o.value = d_value;
+  o.iters = d_iters;
+  o.conv = d_conv;
+  o.pair_a = d_pair_a;
+  o.pair_b = d_pair_b;
+  return gram_shard_run(c, rank, world, tol, max_iter, npairs_out, &o);
+}
+
+int mgk_gram_assemble(int device, int64_t npairs, const int32_t* d_pair_a, const int32_t* d_pair_b,
+                      const double* d_value, const int32_t* d_iters, const uint8_t* d_conv, int64_t G, double* d_K,
+                      int32_t* d_K_iters, uint8_t* d_K_conv) {
+  if (npairs < 0 || G < 0) return fail(MGK_E_INVALID, "negative size");
+  if (npairs > 0 && (!d_pair_a || !d_pair_b || !d_conv || (d_K && !d_value) || (d_K_iters && !d_iters)))
+    return fail(MGK_E_INVALID, "null record array");
+  CUDA_TRY(cudaSetDevice(device));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaStream_t s;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaError_t e = launch_gram_assemble(npairs, d_pair_a, d_pair_b, d_value, d_iters, d_conv, G, d_K, d_K_iters,
+                                       d_K_conv, sms, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (e != cudaSuccess) return fail(MGK_E_CUDA, "gram assembly: %s", cudaGetErrorString(e));
+  return MGK_OK;
+}
+
+int mgk_gram_multi(mgk_ctx* const* ctxs, int nctx, double tol, int64_t max_iter, double* K, int32_t* iters,
+                   uint8_t* conv) {
+  if (!ctxs || nctx < 1) return fail(MGK_E_INVALID, "need at least one context");
+  for (int k = 0; k < nctx; ++k) {
+    if (!ctxs[k]) return fail(MGK_E_INVALID, "null context %d", k);
+    if (!ctxs[k]->uploaded) return fail(MGK_E_STATE, "context %d has no dataset", k);
+    if (ctxs[k]->G != ctxs[0]->G) return fail(MGK_E_INVALID, "contexts hold different datasets");
+  }
+  const int64_t G = ctxs[0]->G;
+  // one host thread per context: solve shard k of nctx, copy the compact records back, scatter them
+  // (mirrored, NaN where not converged) into the caller's matrices -- shards are disjoint pair sets,
+  // so the threads never write the same entry
+  std::vector<int> rcs(nctx, MGK_OK);
+  std::vector<std::string> errs(nctx);
+  std::vector<double> ms(nctx, 0.0);
+  std::vector<int> launches(nctx, 0);
+  auto work = [&](int k) {
+    mgk_ctx* c = ctxs[k];
+    cudaSetDevice(c->device);
+    std::vector<int32_t> pa, pb, it;
+    std::vector<double> v;
+    std::vector<uint8_t> cv;
+    int64_t n = 0;
+    int rc = mgk_gram_shard(c, k, nctx, tol, max_iter, &n, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (!rc) {
+      pa.resize(n);
+      pb.resize(n);
+      v.resize(n);
+      it.resize(n);
+      cv.resize(n);
+      rc = mgk_gram_shard(c, k, nctx, tol, max_iter, &n, pa.data(), pb.data(), v.data(), it.data(), cv.data());
+    }
+    rcs[k] = rc;
+    if (rc) {
+      errs[k] = g_err;
+      return;
+    }
+    ms[k] = c->last_ms;
+    launches[k] = c->last_launches;
+    for (int64_t q = 0; q < n; ++q) {
+      const int64_t a = pa[q], b = pb[q];
+      const double kv = cv[q] ? v[q] : std::numeric_limits<double>::quiet_NaN();
+      if (K) K[a * G + b] = K[b * G + a] = kv;
+      if (iters) iters[a * G + b] = iters[b * G + a] = it[q];
+      if (conv) conv[a * G + b] = conv[b * G + a] = cv[q];
+    }
+  };
+  std::vector<std::thread> th;
+  for (int k = 1; k < nctx; ++k) th.emplace_back(work, k);
+  work(0);
+  for (auto& t : th) t.join();
+  for (int k = 0; k < nctx; ++k)
+    if (rcs[k]) return fail(rcs[k], "device %d: %s", ctxs[k]->device, errs[k].c_str());
+  // device time of the group = the slowest shard (max over devices); launches summed
+  const double mx = *std::max_element(ms.begin(), ms.end());
+  int nl = 0;
+  for (int x : launches) nl += x;
+  for (int k = 0; k < nctx; ++k) {
+    ctxs[k]->last_ms = mx;
+    ctxs[k]->last_launches = nl;
+  }
   return MGK_OK;
 }
 
@@ -1614,8 +1725,8 @@ int mgk_counters(mgk_ctx* c, int32_t a, int32_t b, int64_t applies, const double
 }
 
 int mgk_transfer_bytes(int64_t* h2d, int64_t* d2h_out) {
-  if (h2d) *h2d = g_h2d_bytes;
-  if (d2h_out) *d2h_out = g_d2h_bytes;
+  if (h2d) *h2d = g_h2d_bytes.load();
+  if (d2h_out) *d2h_out = g_d2h_bytes.load();
   return MGK_OK;
 }
 

@@ -51,7 +51,8 @@ struct WarpSmem {
   float T[UNLAB ? NU : 1][32];
   float X[NODEWISE ? NU : 1][32];
   float4 UE[SMAX];        // U nonzeros in row order: {weight form, label, byte offset of P row j, -}
-  float SEG[2 * 32 * SLM];  // segment sums of two U-rows
+  static constexpr int kRowsPerPass = SLM <= 4 ? 4 : 2;
+  float SEG[kRowsPerPass * 32 * SLM];  // slot products of the U-rows of one pass, segment-summed per L row
   int urow[NU + 8];
   int lrow[40];
   float upq[NU];          // p_i of U nodes
@@ -122,25 +123,30 @@ __device__ __forceinline__ double shifted_diag(const DatasetDev& ds, double diag
 // reference's iteration counts.
 //
 // The matvec uses the warp solver's lane-slot mapping: the warp walks the
-// rows of U (the graph with more nonzeros) in lock step, lane l owns the
-// nonzeros l + 32 t of L (t < NS <= 4: min(n, m) <= 11 gives S_L <= 110), so
-// every lane runs the same trip counts -- no divergent per-element loops.
+// rows of U in lock step, lane l owns the nonzeros l + 32 t of L (t < NS), so
+// every lane runs the same trip counts -- no divergent per-element loops.  U is
+// the graph with FEWER nodes (n m <= 128 gives n_U <= 11): few row passes (each
+// ends in a warp sync and a segment sum) and up to NS = 10 independent slot
+// chains per U nonzero.
 // The field lives compactly as [i * m + l] (a warp-uniform row j gathers
 // P[j * m + col_L(t)], consecutive banks); the vector phase gives lane e % 32
 // the elements e (<= 4 per lane).
 // ---------------------------------------------------------------------------
 constexpr int kTinyMax = 128;
-constexpr int kTinySlots = 4;
+constexpr int kTinySlots = SLOTS;  // lane graph of <= 320 nonzeros (the small class)
+constexpr int kTinyRows = 11;      // n_U <= floor(128 / 11)... U is the smaller graph: n_U^2 <= n_U n_L <= 128
 
 struct TinySmem {
   double P[kTinyMax];
   double AP[kTinyMax];
-  double DG[kTinyMax];
+  double RD[kTinyMax];  // 1 / diag (Jacobi preconditioner)
   double SS[kTinyMax];
+  double R[kTinyMax];   // residual and iterate (shared memory keeps the matvec's registers free)
+  double X[kTinyMax];
   double SEG[2 * 32 * kTinySlots];  // slot products of two U rows, segment-summed per L row
-  float4 UE[SMAX];                  // U nonzeros: {weight form, label, P row offset j * m, -}
-  int urow[NU + 8];
-  int lrow[40];
+  float4 UE[kTinyRows * (kTinyRows - 1)];  // U nonzeros: {weight form, label, P row offset j * m, -}
+  int urow[kTinyRows + 1];
+  int lrow[NU + 8];
 };
 
 // AP = SS * P - OFF for all U rows; OFF[i][l] = sum_{k in U(i)} sum_{t in L(l)} kappa w_k w'_t P[j_k][col_t]
@@ -162,14 +168,38 @@ __device__ __forceinline__ void tiny_xmv(TinySmem& S, const KernelDesc& ek, int 
       double pc[NS];
 #pragma unroll
       for (int t = 0; t < NS; ++t) pc[t] = LAP ? S.P[row * m + lrw[t]] : 0.0;
-      for (int k = S.urow[row]; k < S.urow[row + 1]; ++k) {
-        const float4 e = S.UE[k];
-        const double* pr = S.P + __float_as_int(e.z);
+      // narrow lane graphs: two nonzeros per step into independent accumulators (the FP64 FMA chains
+      // overlap); from 3 slots on the slots themselves supply the independent chains
+      constexpr bool kPairK = NS <= 2;
+      double acc2[kPairK ? NS : 1];
+#pragma unroll
+      for (int t = 0; t < (kPairK ? NS : 1); ++t) acc2[t] = 0.0;
+      const int k1 = S.urow[row + 1];
+      int k = S.urow[row];
+      for (; kPairK && k + 1 < k1; k += 2) {
+        const float4 e0 = S.UE[k], e1 = S.UE[k + 1];
+        const double* p0 = S.P + __float_as_int(e0.z);
+        const double* p1 = S.P + __float_as_int(e1.z);
 #pragma unroll
         for (int t = 0; t < NS; ++t) {
-          const double pv = LAP ? pr[lcol[t]] - pc[t] : pr[lcol[t]];
-          acc[r][t] = fma((double)edge_kappa_w<EK>(ek, e.y, llab[t], e.x), pv, acc[r][t]);
+          const double v0 = LAP ? p0[lcol[t]] - pc[t] : p0[lcol[t]];
+          const double v1 = LAP ? p1[lcol[t]] - pc[t] : p1[lcol[t]];
+          acc[r][t] = fma((double)edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), v0, acc[r][t]);
+          if constexpr (kPairK) acc2[t] = fma((double)edge_kappa_w<EK>(ek, e1.y, llab[t], e1.x), v1, acc2[t]);
         }
+      }
+      for (; k < k1; ++k) {
+        const float4 e0 = S.UE[k];
+        const double* p0 = S.P + __float_as_int(e0.z);
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+          const double v0 = LAP ? p0[lcol[t]] - pc[t] : p0[lcol[t]];
+          acc[r][t] = fma((double)edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), v0, acc[r][t]);
+        }
+      }
+      if constexpr (kPairK) {
+#pragma unroll
+        for (int t = 0; t < NS; ++t) acc[r][t] += acc2[t];
       }
     }
 #pragma unroll
@@ -198,10 +228,11 @@ __device__ __forceinline__ void tiny_xmv_dispatch(int ns, TinySmem& S, const Ker
                                                   const int (&lrw)[kTinySlots], const float (&lw)[kTinySlots],
                                                   const float (&llab)[kTinySlots], int lr0, int lr1) {
   switch (ns) {
-    case 1: tiny_xmv<1, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
-    case 2: tiny_xmv<2, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
-    case 3: tiny_xmv<3, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
-    case 4: tiny_xmv<4, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
+#define MGK_TINY_CASE(N) \
+    case N: tiny_xmv<N, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
+    MGK_TINY_CASE(1) MGK_TINY_CASE(2) MGK_TINY_CASE(3) MGK_TINY_CASE(4) MGK_TINY_CASE(5)
+    MGK_TINY_CASE(6) MGK_TINY_CASE(7) MGK_TINY_CASE(8) MGK_TINY_CASE(9) MGK_TINY_CASE(10)
+#undef MGK_TINY_CASE
     default:  // edgeless L: OFF = 0 (an edgeless U has no rows to walk either)
       for (int e = lane; e < nu * m; e += 32) S.AP[e] = S.SS[e] * S.P[e];
       __syncwarp();
@@ -242,7 +273,6 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
     }
   }
   const int lr0 = lane < m ? S.lrow[lane] : 0, lr1 = lane < m ? S.lrow[lane + 1] : 0;
-  double r[4], x[4];
   double bb_u = 0.0, bb_l = 0.0;
   if (lane < nu) {
     double dq = ds.deg[U.node_off + lane] * ds.q64[U.node_off + lane];
@@ -256,16 +286,15 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     const int e = lane + 32 * s;
-    r[s] = 0.0;
-    x[s] = 0.0;
     if (e < nm) {
       const int i = e / m, l = e - i * m;
       const int64_t vu = U.node_off + i, vl = L.node_off + l;
       const double dg = diag_of(ds, vk, prm, out, vlab, vu, vl);
       const double b = (ds.deg[vu] * ds.q64[vu]) * (ds.deg[vl] * ds.q64[vl]);
-      S.DG[e] = dg;
+      S.RD[e] = 1.0 / dg;
       S.SS[e] = lap ? shifted_diag(ds, dg, vu, vl) : dg;
-      r[s] = b;
+      S.R[e] = b;
+      S.X[e] = 0.0;
       const double z = b / dg;
       S.P[e] = z;
       rho += b * z;
@@ -297,10 +326,11 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
       if (e < nm) {
-        x[s] += alpha * S.P[e];
-        r[s] -= alpha * S.AP[e];
-        rr_l += r[s] * r[s];
-        rz_l += r[s] * (r[s] / S.DG[e]);
+        S.X[e] += alpha * S.P[e];
+        const double r = S.R[e] - alpha * S.AP[e];
+        S.R[e] = r;
+        rr_l += r * r;
+        rz_l += r * (r * S.RD[e]);
       }
     }
     rr = warp_sum(rr_l);
@@ -314,7 +344,7 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int e = lane + 32 * s;
-      if (e < nm) S.P[e] = r[s] / S.DG[e] + beta * S.P[e];
+      if (e < nm) S.P[e] = S.R[e] * S.RD[e] + beta * S.P[e];
     }
     rho = rho_next;
     __syncwarp();
@@ -325,8 +355,8 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
     const int e = lane + 32 * s;
     if (e < nm) {
       const int i = e / m, l = e - i * m;
-      val += (double)ds.p[U.node_off + i] * (double)ds.p[L.node_off + l] * x[s];
-      if (nw) nw[swap ? (int64_t)l * nu + i : (int64_t)e] = (float)x[s];
+      val += (double)ds.p[U.node_off + i] * (double)ds.p[L.node_off + l] * S.X[e];
+      if (nw) nw[swap ? (int64_t)l * nu + i : (int64_t)e] = (float)S.X[e];
     }
   }
   value_out = warp_sum(val);
@@ -371,35 +401,36 @@ __device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& 
   }
 }
 
-// Two U-rows per pass: one SEG round trip and one pair of warp syncs per two
-// rows, and two independent summation chains in the segment reduction.
+// kRowsPerPass U-rows per pass: one SEG round trip and one pair of warp syncs per
+// pass, and kRowsPerPass independent summation chains in the segment reduction.
 template <int NS, int EK, int SLM, class Smem>
 __device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int nu, int m, int lane,
                                             const int (&lcoff)[SLM], const float (&lw)[SLM],
                                             const float (&llab)[SLM], int lr0, int lr1) {
+  constexpr int RP = Smem::kRowsPerPass;
   const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
-  for (int i = 0; i < nu; i += 2) {
-    const bool two = i + 1 < nu;
-    float acc0[NS], acc1[NS];
+  for (int i = 0; i < nu; i += RP) {
 #pragma unroll
-    for (int t = 0; t < NS; ++t) acc0[t] = acc1[t] = 0.0f;
-    accumulate_row<NS, EK, SLM>(S, ek, i, pbase, lcoff, llab, acc0);
-    if (two) accumulate_row<NS, EK, SLM>(S, ek, i + 1, pbase, lcoff, llab, acc1);
+    for (int r = 0; r < RP; ++r) {
+      float acc[NS];
 #pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      S.SEG[lane + 32 * t] = acc0[t] * lw[t];
-      S.SEG[32 * SLM + lane + 32 * t] = acc1[t] * lw[t];
+      for (int t = 0; t < NS; ++t) acc[t] = 0.0f;
+      if (i + r < nu) accumulate_row<NS, EK, SLM>(S, ek, i + r, pbase, lcoff, llab, acc);
+#pragma unroll
+      for (int t = 0; t < NS; ++t) S.SEG[32 * SLM * r + lane + 32 * t] = acc[t] * lw[t];
     }
     __syncwarp();
     if (lane < m) {
-      float s0 = 0.0f, s1 = 0.0f;
-#pragma unroll 2
+      float sr[RP];
+#pragma unroll
+      for (int r = 0; r < RP; ++r) sr[r] = 0.0f;
       for (int q = lr0; q < lr1; ++q) {
-        s0 += S.SEG[q];
-        s1 += S.SEG[32 * SLM + q];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) sr[r] += S.SEG[32 * SLM * r + q];
       }
-      S.OFF[i][lane] = s0;
-      if (two) S.OFF[i + 1][lane] = s1;
+#pragma unroll
+      for (int r = 0; r < RP; ++r)
+        if (i + r < nu) S.OFF[i + r][lane] = sr[r];
     }
     __syncwarp();
   }
@@ -660,7 +691,10 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       }
       ++it;
       // ---------------- PCG update (solver.py:98-110); A p = diag * p - OFF
-      double pap = 0.0, pxp = 0.0;
+      // Dot products: FP32 partial sums of two rows, promoted to FP64 once per pair of rows (halves the
+      // F2F conversions, which share the XU pipe with MUFU.EX2); px . p (value only) in FP32 per lane.
+      double pap = 0.0;
+      float pend = 0.0f, pxp32 = 0.0f;
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
         if (i >= nu) break;  // warp-uniform: no issue slots spent on absent rows
@@ -668,16 +702,22 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
           const float p = S.P[i][lane];
           const float ap = fmaf(dv[i], p, -S.OFF[i][lane]);
           S.OFF[i][lane] = ap;
-          pap += (double)p * (double)ap;
-          pxp += (double)S.upq[i] * (double)p;
+          if (i & 1) {
+            pap += (double)fmaf(p, ap, pend);
+            pend = 0.0f;
+          } else {
+            pend = p * ap;
+          }
+          pxp32 = fmaf(S.upq[i], p, pxp32);
         }
       }
-      pap = warp_sum(pap);
-      pxp = warp_sum(pxp * (double)lp);
+      pap = warp_sum(pap + (double)pend);
+      const double pxp = warp_sum((double)pxp32 * (double)lp);
       const double alpha = rho / pap;
       value += alpha * pxp;  // px . x accumulated as sum_k alpha_k (px . p_k)
       const float af = (float)alpha;
       double rr_l = 0.0, rz_l = 0.0;
+      float rr_p = 0.0f, rz_p = 0.0f;
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
         if (i >= nu) break;  // warp-uniform: no issue slots spent on absent rows
@@ -688,12 +728,18 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
           const float z = r * rcp_approx(UNLAB && lap ? fmaf(S.udm[i], lbm, dv[i]) : dv[i]);
           rv[i] = r;
           S.OFF[i][lane] = z;
-          rr_l += (double)r * (double)r;
-          rz_l += (double)r * (double)z;
+          if (i & 1) {
+            rr_l += (double)fmaf(r, r, rr_p);
+            rz_l += (double)fmaf(r, z, rz_p);
+            rr_p = rz_p = 0.0f;
+          } else {
+            rr_p = r * r;
+            rz_p = r * z;
+          }
         }
       }
-      rr = warp_sum(rr_l);
-      const double rho_next = warp_sum(rz_l);
+      rr = warp_sum(rr_l + (double)rr_p);
+      const double rho_next = warp_sum(rz_l + (double)rz_p);
       if (rr < eps) {
         conv = true;
         break;
@@ -724,7 +770,7 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
 
 // Tiny-pair kernel: warp per pair, FP64 vectors (see solve_tiny).
 template <int EK>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
 k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams prm, SolveOut out,
            unsigned long long* queue) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -738,9 +784,8 @@ k_pcg_tiny(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int32_t ga, gb;
     decode_pair(job, (int64_t)pid, ga, gb);
     const GraphDesc A = ds.graphs[ga], B = ds.graphs[gb];
-    // U = the graph with more nonzeros (rows walked by the warp), L = the other (lane slots); the
-    // smaller node count bounds S_L <= 110 <= 32 * kTinySlots
-    const bool swap = (2 * B.ne > 2 * A.ne) || (B.ne == A.ne && B.n > A.n);
+    // U = the graph with fewer nodes (rows walked by the warp), L = the other (lane slots, small class)
+    const bool swap = (B.n < A.n) || (B.n == A.n && B.ne < A.ne);
     const GraphDesc U = swap ? B : A, L = swap ? A : B;
     {  // rows from the dataset's row expansion of the octiles (see k_pcg_warp)
       const float4* ur = ds.rowent + U.nz_off;

@@ -43,6 +43,9 @@ SIGNATURES = {
     "mgk_bench_peaks": (C.c_int, [C.c_int, _P, _P]),
     "mgk_transfer_bytes": (C.c_int, [_P, _P]),
     "mgk_counters": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _P, _P, C.c_int, _P]),
+    "mgk_gram_shard_device": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, _P, _P, _P, _P, _P, _P]),
+    "mgk_gram_assemble": (C.c_int, [C.c_int, C.c_int64, _P, _P, _P, _P, _P, C.c_int64, _P, _P, _P]),
+    "mgk_gram_multi": (C.c_int, [_P, C.c_int, C.c_double, C.c_int64, _P, _P, _P]),
 }
 
 
@@ -238,6 +241,15 @@ class Context:
                                  _ptr(res), _ptr(cv), _ptr(nw)))
         return val, it, res, cv.astype(bool), nw
 
+    def gram_shard_device(self, rank: int, world: int, tol: float, max_iter: int = 0, out=None) -> int:
+        """mgk_gram_shard_device: out = (pair_a, pair_b, value, iters, conv) device tensors (torch) on this
+        context's device, or None to count the shard's pairs."""
+        n = C.c_int64()
+        ptrs = [C.c_void_p(t.data_ptr()) for t in out] if out is not None else [None] * 5
+        check(self.lib.mgk_gram_shard_device(self.h, int(rank), int(world), float(tol), int(max_iter), C.byref(n),
+                                             *ptrs))
+        return n.value
+
     def counters(self, a: int, b: int, applies: int, model, thresholds, force_dense: bool) -> np.ndarray:
         """mgk_counters: {flops, t1_load, t1_store, t2_load, t2_store, tile_pairs} after `applies` applies."""
         m = np.array([model.E, model.F, model.X, model.r], dtype=np.float64)
@@ -338,3 +350,24 @@ class PackedDataset:
         data = [np.asarray(lab, np.float64).reshape(-1, d) if lab is not None else np.zeros((c, d))
                 for lab, c in zip(labs, counts)]
         return LABEL_VEC, d, np.ascontiguousarray(np.concatenate(data).reshape(-1), dtype=np.float64)
+
+
+def gram_multi(ctxs: list, tol: float, max_iter: int = 0):
+    """mgk_gram_multi: one host process, one context per device; returns (K, iterations, converged)."""
+    lib = load()
+    G = ctxs[0].G
+    K = np.empty((G, G), dtype=np.float64)
+    it = np.empty((G, G), dtype=np.int32)
+    cv = np.empty((G, G), dtype=np.uint8)
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    check(lib.mgk_gram_multi(arr, len(ctxs), float(tol), int(max_iter), _ptr(K), _ptr(it), _ptr(cv)))
+    return K, it, cv.astype(bool)
+
+
+def gram_assemble(device: int, records, G: int, K=None, iters=None, conv=None):
+    """mgk_gram_assemble on device tensors: records = (pair_a, pair_b, value, iters, conv)."""
+    lib = load()
+    pa, pb, v, it, cv = records
+    p = lambda t: None if t is None else C.c_void_p(t.data_ptr())  # noqa: E731
+    check(lib.mgk_gram_assemble(int(device), int(pa.numel()), p(pa), p(pb), p(v), p(it), p(cv), int(G), p(K),
+                                p(iters), p(conv)))

@@ -598,3 +598,64 @@ def test_pbr_protein_shaped_vs_oracle(mgk):
     perms = mgk.pbr_reorder_many(graphs, seed=5)
     for g, p in zip(graphs, perms):
         assert p.forward.tolist() == O.pbr_reorder(g, 5).tolist()
+
+
+def _mixed_dataset(mgk, seed):
+    from paper_1910_06310_b200 import synth
+
+    rng = np.random.default_rng(seed)
+    ii, jj = np.triu_indices(20, 1)
+    k20 = mgk.LabeledGraph.from_arrays(20, ii, jj, rng.uniform(0.2, 2.0, ii.size), node_labels=rng.integers(0, 4, 20),
+                                       edge_labels=rng.uniform(0, 2, ii.size))
+    return [synth.molecule(rng, int(n)) for n in rng.integers(2, 24, size=30)] + \
+           [synth.molecule(rng, int(n)) for n in (30, 45, 60)] + [k20]
+
+
+def test_gram_multi_device_bit_identical(mgk):
+    """compute_gram(devices=[...]) (mgk_gram_multi: one process, one context + host thread per device,
+    round-robin cost-ordered shards scattered into the host matrix) reproduces the single-device Gram
+    bit for bit -- here with 2 and 3 contexts on the one GPU of the test box."""
+    ds = _mixed_dataset(mgk, 51)
+    ref = mgk.compute_gram(ds, "delta:0.5", "se:1.0")
+    for devs in ([0, 0], [0, 0, 0]):
+        res = mgk.compute_gram(ds, "delta:0.5", "se:1.0", devices=devs)
+        assert np.array_equal(res.matrix, ref.matrix), devs
+        assert np.array_equal(res.iterations, ref.iterations) and np.array_equal(res.converged, ref.converged)
+    res = mgk.compute_gram(ds, "delta:0.5", "se:1.0", devices=[0, 0], normalize=True)
+    assert np.allclose(res.matrix, mgk.normalize_gram(ref.matrix), rtol=1e-15, atol=0)
+
+
+def test_gram_shard_device_records_assemble(mgk):
+    """mgk_gram_shard_device writes each shard's records to caller-owned device tensors (the input of the
+    NCCL gather in bench.py), mgk_gram_assemble scatters the concatenated records into a device Gram:
+    identical to the single-device matrix, padding records (id -1) ignored."""
+    import torch
+
+    from paper_1910_06310_b200 import native
+    from paper_1910_06310_b200.solver import context
+
+    ds = _mixed_dataset(mgk, 52)
+    ref = mgk.compute_gram(ds, "delta:0.5", "se:1.0")
+    ctx = context(0)
+    ctx.upload(native.PackedDataset(ds))
+    ctx.set_kernels("delta:0.5", "se:1.0")
+    dev = torch.device("cuda", 0)
+    parts = []
+    for rank in range(3):
+        n = ctx.gram_shard_device(rank, 3, 1e-10)
+        rec = (torch.empty(n + 2, dtype=torch.int32, device=dev), torch.empty(n + 2, dtype=torch.int32, device=dev),
+               torch.empty(n + 2, dtype=torch.float64, device=dev), torch.empty(n + 2, dtype=torch.int32, device=dev),
+               torch.zeros(n + 2, dtype=torch.uint8, device=dev))
+        rec[0][n:] = -1  # padding
+        rec[1][n:] = -1
+        assert ctx.gram_shard_device(rank, 3, 1e-10, out=rec) == n
+        parts.append(rec)
+    recs = [torch.cat([p[k] for p in parts]) for k in range(5)]
+    G = len(ds)
+    K = torch.empty((G, G), dtype=torch.float64, device=dev)
+    it = torch.empty((G, G), dtype=torch.int32, device=dev)
+    cv = torch.empty((G, G), dtype=torch.uint8, device=dev)
+    native.gram_assemble(0, recs, G, K, it, cv)
+    assert np.array_equal(K.cpu().numpy(), ref.matrix)
+    assert np.array_equal(it.cpu().numpy(), ref.iterations) and np.array_equal(cv.cpu().numpy().astype(bool),
+                                                                               ref.converged)
