@@ -51,8 +51,7 @@ struct WarpSmem {
   float T[UNLAB ? NU : 1][32];
   float X[NODEWISE ? NU : 1][32];
   float4 UE[SMAX];        // U nonzeros in row order: {weight form, label, byte offset of P row j, -}
-  static constexpr int kRowsPerPass = SLM <= 4 ? 4 : 2;
-  float SEG[kRowsPerPass * 32 * SLM];  // slot products of the U-rows of one pass, segment-summed per L row
+  float SEG[2 * 32 * SLM];  // segment sums of two U-rows
   int urow[NU + 8];
   int lrow[40];
   float upq[NU];          // p_i of U nodes
@@ -401,36 +400,35 @@ __device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& 
   }
 }
 
-// kRowsPerPass U-rows per pass: one SEG round trip and one pair of warp syncs per
-// pass, and kRowsPerPass independent summation chains in the segment reduction.
+// Two U-rows per pass: one SEG round trip and one pair of warp syncs per two
+// rows, and two independent summation chains in the segment reduction.
 template <int NS, int EK, int SLM, class Smem>
 __device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int nu, int m, int lane,
                                             const int (&lcoff)[SLM], const float (&lw)[SLM],
                                             const float (&llab)[SLM], int lr0, int lr1) {
-  constexpr int RP = Smem::kRowsPerPass;
   const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
-  for (int i = 0; i < nu; i += RP) {
+  for (int i = 0; i < nu; i += 2) {
+    const bool two = i + 1 < nu;
+    float acc0[NS], acc1[NS];
 #pragma unroll
-    for (int r = 0; r < RP; ++r) {
-      float acc[NS];
+    for (int t = 0; t < NS; ++t) acc0[t] = acc1[t] = 0.0f;
+    accumulate_row<NS, EK, SLM>(S, ek, i, pbase, lcoff, llab, acc0);
+    if (two) accumulate_row<NS, EK, SLM>(S, ek, i + 1, pbase, lcoff, llab, acc1);
 #pragma unroll
-      for (int t = 0; t < NS; ++t) acc[t] = 0.0f;
-      if (i + r < nu) accumulate_row<NS, EK, SLM>(S, ek, i + r, pbase, lcoff, llab, acc);
-#pragma unroll
-      for (int t = 0; t < NS; ++t) S.SEG[32 * SLM * r + lane + 32 * t] = acc[t] * lw[t];
+    for (int t = 0; t < NS; ++t) {
+      S.SEG[lane + 32 * t] = acc0[t] * lw[t];
+      S.SEG[32 * SLM + lane + 32 * t] = acc1[t] * lw[t];
     }
     __syncwarp();
     if (lane < m) {
-      float sr[RP];
-#pragma unroll
-      for (int r = 0; r < RP; ++r) sr[r] = 0.0f;
+      float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 2
       for (int q = lr0; q < lr1; ++q) {
-#pragma unroll
-        for (int r = 0; r < RP; ++r) sr[r] += S.SEG[32 * SLM * r + q];
+        s0 += S.SEG[q];
+        s1 += S.SEG[32 * SLM + q];
       }
-#pragma unroll
-      for (int r = 0; r < RP; ++r)
-        if (i + r < nu) S.OFF[i + r][lane] = sr[r];
+      S.OFF[i][lane] = s0;
+      if (two) S.OFF[i + 1][lane] = s1;
     }
     __syncwarp();
   }
