@@ -70,10 +70,10 @@ CONFIGS = {
     "3": Config("3", "config3: protein-sized synthetic graphs, {G} graphs n 200..600, shuffled + device PBR, "
                 "all-pairs Gram", "delta:0.5", "se:1.0", 1e-10, 7, True, 48, 6, "k_pcg_panel<SE>"),
     "4": Config("4", "config4: large sparse RGGs, 4 density buckets (mean degree 4/8/16/32) x {B} graphs n 2k..5k, "
-                "shuffled + device PBR, unlabeled, within-bucket Grams", None, None, 1e-6, 3, True, 4, 2,
+                "shuffled + device PBR, unlabeled, within-bucket Grams", None, None, 1e-6, 3, True, 4, 5,
                 "k_pcg_grid<unlabeled>"),
     "4se": Config("4se", "config4 with the SE(1.0) edge kernel on the scaled edge length: 4 buckets x {B} graphs",
-                  None, "se:1.0", 1e-10, 7, True, 0, 0, "k_pcg_grid<SE>"),
+                  None, "se:1.0", 1e-10, 7, True, 0, 2, "k_pcg_grid<SE>"),
     "5": Config("5", "config5: {G} mixed-size synthetic molecules (60% n 4..23, 30% 24..64, 10% 65..128), "
                 "all-pairs Gram", "delta:0.5", "se:1.0", 1e-10, 7, False, 20000, 100, "k_pcg_warp + k_pcg_panel"),
     "5nw": Config("5nw", "config5 nodal similarity: {G} mixed-size molecules, every pair's n_a x n_b field streamed "
@@ -252,12 +252,65 @@ def traffic_from_profiles(cfg: Config):
     return None, None
 
 
+_PERMS = {}
+
+
 def reorder_dataset(ds, device: int):
     """Device PBR (seed 0) of every graph, applied on the host (the public API path)."""
     from paper_1910_06310_b200 import apply_permutation, pbr_reorder_many
 
     perms = pbr_reorder_many(ds, seed=0, device=device)
+    _PERMS[id(ds)] = perms
     return [apply_permutation(g, p) for g, p in zip(ds, perms)]
+
+
+def _oracle_pbr(g):
+    from oracle import mgk_oracle as O
+
+    return O.pbr_reorder(g, seed=0).tolist()
+
+
+def pbr_parity(raw, count: int, max_n: int = 600):
+    """Device PBR permutations of the `count` smallest graphs (n <= max_n) against the oracle restatement
+    (pinned to the reference's forward maps up to n = 600, tests/golden/pbr_large.json), bit for bit."""
+    import multiprocessing as mp
+
+    cand = []
+    for _, ds in raw:
+        perms = _PERMS.get(id(ds))
+        if perms is None:
+            continue
+        cand += [(g.node_count, k, g, perms[k]) for k, g in enumerate(ds) if g.node_count <= max_n]
+    cand = sorted(cand, key=lambda c: (c[0], c[1]))[:count]
+    if not cand:
+        return None
+    with mp.get_context("fork").Pool(min(len(cand), os.cpu_count() or 1)) as pool:
+        ref = pool.map(_oracle_pbr, [c[2] for c in cand])
+    exact = sum(int(c[3].forward.tolist() == r) for c, r in zip(cand, ref))
+    return {"graphs": len(cand), "bit_exact": exact, "nodes": [c[0] for c in cand],
+            "oracle": "oracle/mgk_oracle.pbr_reorder (pinned to the reference's pbr_reorder, n <= 600)"}
+
+
+def _oracle_big_pair(job):
+    from oracle import mgk_oracle as O
+
+    ga, gb, vspec, espec, tol = job
+    system = (O.FactoredSystem(ga, gb, vspec) if espec is None else
+              O.ChunkedSystem(ga, gb, vspec, espec, chunk=512))
+    r = O.solve_pcg(ga, gb, vspec, espec, tol=tol, system=system)
+    return r.value, r.iterations
+
+
+def parity_jobs(cfg, bks):
+    """(bucket, x, y) pairs checked against the oracle: uniform samples, except config 4se, whose
+    full-size SE systems only fit the chunked matrix-free oracle on the smallest graphs -- the smallest
+    graph of the sparsest bucket against itself and against the second smallest."""
+    if cfg.key != "4se":
+        return sample_pairs(bks, cfg.parity_pairs, 1)
+    ds = bks[0][1]
+    order = sorted(range(len(ds)), key=lambda k: (2 * ds[k].edge_count, k))
+    a, b = order[0], order[1]
+    return [(0, a, a), (0, min(a, b), max(a, b))]
 
 
 _T0 = time.perf_counter()
@@ -417,15 +470,24 @@ def run_ours(args, rank, world, local_rank):
             del iu, ju
         worst, it_dev, checked = 0.0, 0, 0
         if cfg.parity_pairs:
+            import multiprocessing as mp
+
             vs, es = _spec(cfg.vspec), _spec(cfg.espec)
-            for b, x, y in sample_pairs(bks, cfg.parity_pairs, 1):
-                ds = bks[b][1]
-                system = O.FactoredSystem(ds[x], ds[y], vs) if es is None else None
-                o = O.solve_pcg(ds[x], ds[y], vs, es, tol=cfg.tol, system=system)
+            jobs = parity_jobs(cfg, bks)
+            big = cfg.key in ("4", "4se")
+            args_ = [(bks[b][1][x], bks[b][1][y], vs, es, cfg.tol) for b, x, y in jobs]
+            if big:
+                with mp.get_context("fork").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+                    refs = pool.map(_oracle_big_pair, args_)
+            else:
+                refs = [(o.value, o.iterations) for o in
+                        (O.solve_pcg(ga, gb, v, e, tol=t) for ga, gb, v, e, t in args_)]
+            for (b, x, y), (ov, oit) in zip(jobs, refs):
                 K, it = Ks[b]
-                worst = max(worst, abs(K[x, y] - o.value) / abs(o.value))
-                it_dev = max(it_dev, abs(int(it[x, y]) - o.iterations))
+                worst = max(worst, abs(K[x, y] - ov) / abs(ov))
+                it_dev = max(it_dev, abs(int(it[x, y]) - oit))
                 checked += 1
+        pbr = pbr_parity(raw, 5) if cfg.reorder else None
         del Ks
         log(f"parity sample done ({checked} pairs)")
         achieved = flops / world / (ms_solve * 1e-3) / 1e12
@@ -527,7 +589,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "parity": {"sample_pairs": checked, "max_rel_err": worst, "max_iter_diff": it_dev,
-                       "bar": "1e-5 relative, +-1 iteration"},
+                       "bar": "1e-5 relative, +-1 iteration", "pbr_permutations": pbr},
             "solve_ms_per_step": ms_solve,
         }
         if per_bucket:
