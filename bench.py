@@ -495,9 +495,14 @@ def run_ours(args, rank, world, local_rank):
 
         # ---- end to end through the public API with host buffers (rank 0)
         e2e_ms = []
-        h0, d0 = ctxs[0].transfer_bytes()
         nrep = max(1, min(args.steps, 3))
-        for _ in range(nrep):
+        # short configs get one untimed warm-up call of the public API path (its first call creates the
+        # process-wide context); the long ones (minutes per call) are timed from their first call
+        plan = ([False] if cfg.key in ("1", "2", "5") else []) + [True] * nrep
+        h0 = d0 = None
+        for timed in plan:
+            if timed and h0 is None:
+                h0, d0 = ctxs[0].transfer_bytes()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             for _, ds in raw:
@@ -510,7 +515,8 @@ def run_ours(args, rank, world, local_rank):
                 res = compute_gram(src, cfg.vspec, cfg.espec, cfg=_solver_cfg(cfg), device=local_rank)
                 assert res.matrix.shape == (len(ds), len(ds))
             torch.cuda.synchronize(dev)
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            if timed:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
         h1, d1 = ctxs[0].transfer_bytes()
         e2e_val = npairs / (float(np.mean(e2e_ms)) * 1e-3)
         log(f"e2e done: {np.mean(e2e_ms):.1f} ms")

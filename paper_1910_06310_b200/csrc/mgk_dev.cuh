@@ -60,8 +60,10 @@ struct GraphDesc {
 //   A p = s * p - sum_{jj'} L_{ii',jj'} (p_jj' - p_ii'),   s in FP64,
 // whose FP32 terms are differences of nearby values.  The cancellation factor
 // diag / s ~ a b / (a + b) with a, b the graphs' max d/q; pairs above
-// kLapFactor (error ~3e-8 x factor without the splitting) switch it on.
-constexpr float kLapFactor = 32.0f;
+// kLapFactor (error ~3e-8 x factor without the splitting, i.e. <= 5e-6 below it) switch it on.
+// Config-4 random geometric graphs at q = 0.05 peak at 143 and keep the cheaper unsplit form (the
+// split factored XMV gathers P twice); datasets past 2 * kPreciseLap run on the FP64 block solver.
+constexpr float kLapFactor = 160.0f;
 
 // Row panels (pcg_panel.cu): consecutive rows whose nonzeros fit 32 lanes x kPanelSlots.
 #ifndef MGK_PANEL_SLOTS

@@ -685,14 +685,95 @@ __device__ long long pair_count(PbrScratch& s, int n, int k, const int* partof, 
 struct PbrGraph {
   int32_t n, S, k;
   int64_t node_off, scratch_off, tile_off, trow_off, nz_off;
+  int64_t cand_stride;  // ints between the two candidates' scratch areas
 };
 
-__global__ void __launch_bounds__(kPbrThreads) k_pbr(const PbrGraph* __restrict__ gs, int G, const Octile* tiles,
-                                                    const int32_t* trow, int* scratch, uint64_t seed,
-                                                    int64_t* forward, int* status) {
+// Adjacency from the octiles: rows in ascending column order == sorted unique neighbours
+__device__ void build_adjacency(PbrScratch& s, const PbrGraph& g, const Octile* tiles, const int32_t* trow) {
+  const int n = g.n;
+  const Octile* t = tiles + g.tile_off;
+  const int32_t* tr = trow + g.trow_off;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int I = i >> 3, r = i & 7;
+    int c = 0;
+    for (int q = tr[I]; q < tr[I + 1]; ++q) c += __popc((uint32_t)(t[q].bitmap >> (8 * r)) & 0xffu);
+    s.tmp[i] = c;
+    s.posmap[i] = -1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < n; ++i) {
+      s.rowptr[i] = acc;
+      acc += s.tmp[i];
+    }
+    s.rowptr[n] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int I = i >> 3, r = i & 7;
+    int pos = s.rowptr[i];
+    for (int q = tr[I]; q < tr[I + 1]; ++q) {
+      const Octile o = t[q];
+      uint32_t byte = (uint32_t)(o.bitmap >> (8 * r)) & 0xffu;
+      for (; byte; byte &= byte - 1) s.adj[pos++] = o.col * 8 + (__ffs(byte) - 1);
+    }
+  }
+  __syncthreads();
+}
+
+// Phase 1: one CTA per (graph, candidate).  Candidate 0 is the natural order, candidate 1 the
+// seeded SplitMix64 shuffle (reorder.py:385-393); each runs recursive bisection + K-way FM in its own
+// scratch and leaves its partition in that scratch's cand[0..n).  The two candidates of a graph are
+// independent, so they run on two SMs at once.
+__global__ void __launch_bounds__(kPbrThreads) k_pbr_cand(const PbrGraph* __restrict__ gs, int G,
+                                                         const Octile* tiles, const int32_t* trow, int* scratch,
+                                                         uint64_t seed, int* status) {
   __shared__ unsigned long long red64[kPbrWarps];
   __shared__ long long redll[kPbrWarps];
   __shared__ int shw[kPbrWarps], shc, shi, shflag;
+  for (int job = blockIdx.x; job < 2 * G; job += gridDim.x) {
+    const int gi = job >> 1, c = job & 1;
+    const PbrGraph g = gs[gi];
+    const int n = g.n, k = g.k;
+    if (k <= 1 || g.S == 0) continue;  // identity (k_pbr_finish)
+    PbrScratch s = carve(scratch + g.scratch_off + c * g.cand_stride, n, g.S, k);
+    build_adjacency(s, g, tiles, trow);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s.order[i] = i;
+    __syncthreads();
+    if (c == 1 && threadIdx.x == 0) {
+      SplitMix64 rng{seed};
+      for (int i = n - 1; i > 0; --i) {
+        const int j = (int)rng.randint((uint64_t)i + 1);
+        const int x = s.order[i];
+        s.order[i] = s.order[j];
+        s.order[j] = x;
+      }
+    }
+    __syncthreads();
+    const long long c0 = clock64();
+    recursive_parts(s, n, k, s.cand, red64, redll, shw, &shc, &shi);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s.dbg[i] = s.cand[i];
+    __syncthreads();
+    const long long c1 = clock64();
+    const bool ok = fm_refine(s, n, k, s.cand, red64, redll, &shflag);
+    const long long c2 = clock64();
+    if (threadIdx.x == 0) {
+      atomicMax(&g_pbr_cycles[0], (unsigned long long)(c1 - c0));
+      atomicMax(&g_pbr_cycles[1], (unsigned long long)(c2 - c1));
+      if (!ok) atomicExch(status, 1);
+    }
+    __syncthreads();
+  }
+}
+
+// Phase 2: one CTA per graph.  The candidate with the smaller Eq. 3 objective wins (natural on ties,
+// reorder.py:394), nodes are ranked by (part, id) (permutation_from_partition, reorder.py:355-358), and
+// the objective / octile-count fallbacks to identity apply (reorder.py:397-403).  Works in candidate
+// 0's scratch (its adjacency is built).
+__global__ void __launch_bounds__(kPbrThreads) k_pbr_finish(const PbrGraph* __restrict__ gs, int G, int* scratch,
+                                                           int64_t* forward) {
+  __shared__ long long redll[kPbrWarps];
   for (int gi = blockIdx.x; gi < G; gi += gridDim.x) {
     const PbrGraph g = gs[gi];
     const int n = g.n, k = g.k;
@@ -702,69 +783,10 @@ __global__ void __launch_bounds__(kPbrThreads) k_pbr(const PbrGraph* __restrict_
       continue;
     }
     PbrScratch s = carve(scratch + g.scratch_off, n, g.S, k);
-    // adjacency from the octiles: rows in ascending column order == sorted unique neighbours
-    const Octile* t = tiles + g.tile_off;
-    const int32_t* tr = trow + g.trow_off;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int I = i >> 3, r = i & 7;
-      int c = 0;
-      for (int q = tr[I]; q < tr[I + 1]; ++q) c += __popc((uint32_t)(t[q].bitmap >> (8 * r)) & 0xffu);
-      s.tmp[i] = c;
-      s.posmap[i] = -1;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int i = 0; i < n; ++i) {
-        s.rowptr[i] = acc;
-        acc += s.tmp[i];
-      }
-      s.rowptr[n] = acc;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int I = i >> 3, r = i & 7;
-      int pos = s.rowptr[i];
-      for (int q = tr[I]; q < tr[I + 1]; ++q) {
-        const Octile o = t[q];
-        uint32_t byte = (uint32_t)(o.bitmap >> (8 * r)) & 0xffu;
-        for (; byte; byte &= byte - 1) s.adj[pos++] = o.col * 8 + (__ffs(byte) - 1);
-      }
-    }
-    __syncthreads();
-    // two candidates: natural order, then the seeded shuffle (reorder.py:385-393)
-    bool ok = true;
-    for (int c = 0; c < 2; ++c) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) s.order[i] = i;
-      __syncthreads();
-      if (c == 1 && threadIdx.x == 0) {
-        SplitMix64 rng{seed};
-        for (int i = n - 1; i > 0; --i) {
-          const int j = (int)rng.randint((uint64_t)i + 1);
-          const int x = s.order[i];
-          s.order[i] = s.order[j];
-          s.order[j] = x;
-        }
-      }
-      __syncthreads();
-      int* cp = s.cand + (int64_t)c * n;
-      const long long c0 = clock64();
-      recursive_parts(s, n, k, cp, red64, redll, shw, &shc, &shi);
-      for (int i = threadIdx.x; i < n; i += blockDim.x) s.dbg[(int64_t)c * n + i] = cp[i];
-      __syncthreads();
-      const long long c1 = clock64();
-      ok &= fm_refine(s, n, k, cp, red64, redll, &shflag);
-      const long long c2 = clock64();
-      if (threadIdx.x == 0) {
-        atomicMax(&g_pbr_cycles[0], (unsigned long long)(c1 - c0));
-        atomicMax(&g_pbr_cycles[1], (unsigned long long)(c2 - c1));
-      }
-    }
-    if (!ok && threadIdx.x == 0) atomicExch(status, 1);
+    const int* cand1 = carve(scratch + g.scratch_off + g.cand_stride, n, g.S, k).cand;
     const long long o0 = pair_count(s, n, k, s.cand, false, redll);
-    const long long o1 = pair_count(s, n, k, s.cand + n, false, redll);
-    const int* best = (o0 <= o1) ? s.cand : s.cand + n;  // min keeps the first on ties
-    // forward: rank nodes by (part, id) (permutation_from_partition, reorder.py:355-358)
+    const long long o1 = pair_count(s, n, k, cand1, false, redll);
+    const int* best = (o0 <= o1) ? s.cand : cand1;  // min keeps the first on ties
     for (int p = threadIdx.x; p < k; p += blockDim.x) s.sizes[p] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&s.sizes[best[i]], 1);
@@ -786,7 +808,6 @@ __global__ void __launch_bounds__(kPbrThreads) k_pbr(const PbrGraph* __restrict_
       s.tmp[i] = s.sizes[P] + r;
     }
     __syncthreads();
-    // fallbacks (reorder.py:397-403): objective and octile count versus identity
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       s.side[i] = s.tmp[i] / kTile;  // parts of the permuted order
       s.locked[i] = i / kTile;       // identity parts
@@ -823,8 +844,9 @@ int pbr_device(int G, const std::vector<int64_t>& node_off, const std::vector<in
     p.tile_off = d.tile_off;
     p.trow_off = d.trow_off;
     p.nz_off = d.nz_off;
+    p.cand_stride = (pbr_scratch_ints(p.n, p.S, p.k) + 31) / 32 * 32;
     gs[g] = p;
-    if (p.k > 1 && p.S > 0) off += (pbr_scratch_ints(p.n, p.S, p.k) + 31) / 32 * 32;
+    if (p.k > 1 && p.S > 0) off += 2 * p.cand_stride;
   }
   (void)edge_off;
   const int64_t nn = node_off[G];
@@ -845,8 +867,12 @@ int pbr_device(int G, const std::vector<int64_t>& node_off, const std::vector<in
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_gs, gs.data(), sizeof(PbrGraph) * G, cudaMemcpyHostToDevice, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_status, 0, sizeof(int), stream);
   if (e == cudaSuccess) {
-    k_pbr<<<G, kPbrThreads, 0, stream>>>(d_gs, G, d_tiles, d_trow, d_scratch, seed, d_fwd, d_status);
+    k_pbr_cand<<<2 * G, kPbrThreads, 0, stream>>>(d_gs, G, d_tiles, d_trow, d_scratch, seed, d_status);
     e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      k_pbr_finish<<<G, kPbrThreads, 0, stream>>>(d_gs, G, d_scratch, d_fwd);
+      e = cudaGetLastError();
+    }
   }
   int status = 0;
   forward.assign(nn, 0);
@@ -864,10 +890,13 @@ int pbr_device(int G, const std::vector<int64_t>& node_off, const std::vector<in
       if (gs[g].k <= 1 || gs[g].S == 0) continue;
       const int n = gs[g].n, S = gs[g].S, k = gs[g].k;
       std::vector<int> cand(2 * n), pre(2 * n);
-      const int64_t cand_off = gs[g].scratch_off + (n + 1) + S + n;
-      const int64_t dbg_off = gs[g].scratch_off + pbr_scratch_ints(n, S, k) - 64 - 2 * (int64_t)n;
-      cudaMemcpy(cand.data(), d_scratch + cand_off, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost);
-      cudaMemcpy(pre.data(), d_scratch + dbg_off, sizeof(int) * pre.size(), cudaMemcpyDeviceToHost);
+      for (int c = 0; c < 2; ++c) {
+        const int64_t base = gs[g].scratch_off + c * gs[g].cand_stride;
+        const int64_t cand_off = base + (n + 1) + S + n;
+        const int64_t dbg_off = base + pbr_scratch_ints(n, S, k) - 64 - 2 * (int64_t)n;
+        cudaMemcpy(cand.data() + c * n, d_scratch + cand_off, sizeof(int) * n, cudaMemcpyDeviceToHost);
+        cudaMemcpy(pre.data() + c * n, d_scratch + dbg_off, sizeof(int) * n, cudaMemcpyDeviceToHost);
+      }
       fprintf(stderr, "PBRDBG %d", g);
       for (int v : cand) fprintf(stderr, " %d", v);
       for (int v : pre) fprintf(stderr, " %d", v);
