@@ -255,13 +255,21 @@ def traffic_from_profiles(cfg: Config):
 _PERMS = {}
 
 
-def reorder_dataset(ds, device: int):
-    """Device PBR (seed 0) of every graph, applied on the host (the public API path)."""
+def reorder_buckets(raw, device: int):
+    """Device PBR (seed 0) of every graph of every bucket in ONE launch (two CTAs per graph, so the
+    wall time is the slowest graph's, not the sum over buckets), applied on the host (the public API
+    path: pbr_reorder_many + apply_permutation)."""
     from paper_1910_06310_b200 import apply_permutation, pbr_reorder_many
 
-    perms = pbr_reorder_many(ds, seed=0, device=device)
-    _PERMS[id(ds)] = perms
-    return [apply_permutation(g, p) for g, p in zip(ds, perms)]
+    allg = [g for _, ds in raw for g in ds]
+    perms = pbr_reorder_many(allg, seed=0, device=device)
+    out, k = [], 0
+    for name, ds in raw:
+        pp = perms[k: k + len(ds)]
+        k += len(ds)
+        _PERMS[id(ds)] = pp
+        out.append((name, [apply_permutation(g, p) for g, p in zip(ds, pp)]))
+    return out
 
 
 def _oracle_pbr(g):
@@ -338,7 +346,7 @@ def run_ours(args, rank, world, local_rank):
     raw = buckets(cfg, args.count)
     log(f"config {cfg.key}: {sum(len(b) for _, b in raw)} graphs synthesised")
     t_pre = time.perf_counter()
-    bks = [(name, reorder_dataset(ds, local_rank) if cfg.reorder else ds) for name, ds in raw]
+    bks = reorder_buckets(raw, local_rank) if cfg.reorder else list(raw)
     reorder_s = time.perf_counter() - t_pre
     if cfg.reorder:
         log(f"device PBR + apply: {reorder_s:.1f} s")
@@ -505,8 +513,8 @@ def run_ours(args, rank, world, local_rank):
                 h0, d0 = ctxs[0].transfer_bytes()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            for _, ds in raw:
-                src = reorder_dataset(ds, local_rank) if cfg.reorder else ds
+            srcs = reorder_buckets(raw, local_rank) if cfg.reorder else raw
+            for (_, ds), (_, src) in zip(raw, srcs):
                 if cfg.nodewise:
                     got = stream_nodewise(src, _checksum, cfg.vspec, cfg.espec, _solver_cfg(cfg), NW_CHUNK,
                                           device=local_rank)

@@ -82,17 +82,8 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
                                                const float (&llab)[NS], float (&acc)[NS],
                                                const float (&pc)[NS]) {
   int k = k0;
-  // the row entries of the next pair of nonzeros are loaded one step ahead, so their latency overlaps
-  // the current step's P gathers and edge-kernel evaluations (two dependent loads per contribution
-  // otherwise: the entry, then the P element it addresses)
-  float4 n0 = k + 1 < k1 ? ue[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-  float4 n1 = k + 1 < k1 ? ue[k + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
   for (; k + 1 < k1; k += 2) {
-    const float4 e0 = n0, e1 = n1;
-    if (k + 3 < k1) {
-      n0 = ue[k + 2];
-      n1 = ue[k + 3];
-    }
+    const float4 e0 = ue[k], e1 = ue[k + 1];
     const float* r0 = P + __float_as_int(e0.x) * m;
     const float* r1 = P + __float_as_int(e1.x) * m;
     float p0[NS], p1[NS];

@@ -15,7 +15,7 @@ while [ $# -ge 2 ]; do
   $NVCC $FL -DMGK_PANEL_THREADS=512 -DMGK_PANEL_NS=p512 $defs -c csrc/pcg_panel.cu -o build/$name/pcg_panel_512.o &
   wait
   objs="build/$name/capi.o build/$name/pcg_panel_256.o build/$name/pcg_panel_512.o"
-  for f in tiles pcg_warp pcg_block pbr bench_support gram_post ingest; do objs="$objs build/$f.o"; done
+  for f in tiles pcg_warp pcg_block pbr bench_support gram_post ingest order; do objs="$objs build/$f.o"; done
   $NVCC -gencode arch=compute_100a,code=sm_100a -shared -o libmgk_$name.so $objs -lcudart
   echo built libmgk_$name.so
 done
