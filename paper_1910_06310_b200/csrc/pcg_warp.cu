@@ -149,69 +149,61 @@ struct TinySmem {
 };
 
 // AP = SS * P - OFF for all U rows; OFF[i][l] = sum_{k in U(i)} sum_{t in L(l)} kappa w_k w'_t P[j_k][col_t]
-// (Laplacian splitting: P[j_k][col_t] - P[i][l] instead of P[j_k][col_t]).
+// (Laplacian splitting: P[j_k][col_t] - P[i][l] instead of P[j_k][col_t]).  Lane slot t holds an
+// undirected L edge {l_t, c_t}: one edge-kernel value (MUFU.EX2 + F2F) feeds the contributions of
+// both directed entries l_t -> c_t (gathers P[j][c_t], lands on OFF[i][l_t]) and c_t -> l_t
+// (gathers P[j][l_t], lands on OFF[i][c_t]); the per-entry accumulation order is unchanged.
 template <int NS, int EK, bool LAP>
 __device__ __forceinline__ void tiny_xmv(TinySmem& S, const KernelDesc& ek, int nu, int m, int lane,
                                          const int (&lcol)[kTinySlots], const int (&lrw)[kTinySlots],
-                                         const float (&lw)[kTinySlots], const float (&llab)[kTinySlots], int lr0,
-                                         int lr1) {
+                                         const int (&lkab)[kTinySlots], const float (&lw)[kTinySlots],
+                                         const float (&llab)[kTinySlots], int nund, int lr0, int lr1) {
   for (int i = 0; i < nu; i += 2) {
     const bool two = i + 1 < nu;
-    double acc[2][NS];
+    double acc[2][NS], accb[2][NS];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
 #pragma unroll
-      for (int t = 0; t < NS; ++t) acc[r][t] = 0.0;
+      for (int t = 0; t < NS; ++t) acc[r][t] = accb[r][t] = 0.0;
       if (r == 1 && !two) break;
       const int row = i + r;
-      double pc[NS];
+      double pca[NS], pcb[NS];
 #pragma unroll
-      for (int t = 0; t < NS; ++t) pc[t] = LAP ? S.P[row * m + lrw[t]] : 0.0;
-      // narrow lane graphs: two nonzeros per step into independent accumulators (the FP64 FMA chains
-      // overlap); from 3 slots on the slots themselves supply the independent chains
-      constexpr bool kPairK = NS <= 2;
-      double acc2[kPairK ? NS : 1];
-#pragma unroll
-      for (int t = 0; t < (kPairK ? NS : 1); ++t) acc2[t] = 0.0;
-      const int k1 = S.urow[row + 1];
-      int k = S.urow[row];
-      for (; kPairK && k + 1 < k1; k += 2) {
-        const float4 e0 = S.UE[k], e1 = S.UE[k + 1];
-        const double* p0 = S.P + __float_as_int(e0.z);
-        const double* p1 = S.P + __float_as_int(e1.z);
-#pragma unroll
-        for (int t = 0; t < NS; ++t) {
-          const double v0 = LAP ? p0[lcol[t]] - pc[t] : p0[lcol[t]];
-          const double v1 = LAP ? p1[lcol[t]] - pc[t] : p1[lcol[t]];
-          acc[r][t] = fma((double)edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), v0, acc[r][t]);
-          if constexpr (kPairK) acc2[t] = fma((double)edge_kappa_w<EK>(ek, e1.y, llab[t], e1.x), v1, acc2[t]);
-        }
+      for (int t = 0; t < NS; ++t) {
+        pca[t] = LAP ? S.P[row * m + lrw[t]] : 0.0;  // l -> c lands on (row, l)
+        pcb[t] = LAP ? S.P[row * m + lcol[t]] : 0.0;  // c -> l lands on (row, c)
       }
-      for (; k < k1; ++k) {
+      const int k1 = S.urow[row + 1];
+      for (int k = S.urow[row]; k < k1; ++k) {
         const float4 e0 = S.UE[k];
         const double* p0 = S.P + __float_as_int(e0.z);
 #pragma unroll
         for (int t = 0; t < NS; ++t) {
-          const double v0 = LAP ? p0[lcol[t]] - pc[t] : p0[lcol[t]];
-          acc[r][t] = fma((double)edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), v0, acc[r][t]);
+          const double c = (double)edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x);
+          const double va = LAP ? p0[lcol[t]] - pca[t] : p0[lcol[t]];
+          const double vb = LAP ? p0[lrw[t]] - pcb[t] : p0[lrw[t]];
+          acc[r][t] = fma(c, va, acc[r][t]);
+          accb[r][t] = fma(c, vb, accb[r][t]);
         }
-      }
-      if constexpr (kPairK) {
-#pragma unroll
-        for (int t = 0; t < NS; ++t) acc[r][t] += acc2[t];
       }
     }
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
-      S.SEG[lane + 32 * t] = acc[0][t] * (double)lw[t];
-      S.SEG[32 * NS + lane + 32 * t] = acc[1][t] * (double)lw[t];
+      if (lane + 32 * t < nund) {
+        const int ka = lkab[t] & 0xffff, kb = lkab[t] >> 16;
+        const double w = (double)lw[t];
+        S.SEG[ka] = acc[0][t] * w;
+        S.SEG[kb] = accb[0][t] * w;
+        S.SEG[32 * kTinySlots + ka] = acc[1][t] * w;
+        S.SEG[32 * kTinySlots + kb] = accb[1][t] * w;
+      }
     }
     __syncwarp();
     if (lane < m) {
       double s0 = 0.0, s1 = 0.0;
       for (int q = lr0; q < lr1; ++q) {
         s0 += S.SEG[q];
-        s1 += S.SEG[32 * NS + q];
+        s1 += S.SEG[32 * kTinySlots + q];
       }
       const int e0 = i * m + lane;
       S.AP[e0] = S.SS[e0] * S.P[e0] - s0;
@@ -222,15 +214,14 @@ __device__ __forceinline__ void tiny_xmv(TinySmem& S, const KernelDesc& ek, int 
 }
 
 template <int EK, bool LAP>
-__device__ __forceinline__ void tiny_xmv_dispatch(int ns, TinySmem& S, const KernelDesc& ek, int nu, int m,
-                                                  int lane, const int (&lcol)[kTinySlots],
-                                                  const int (&lrw)[kTinySlots], const float (&lw)[kTinySlots],
-                                                  const float (&llab)[kTinySlots], int lr0, int lr1) {
-  switch (ns) {
+__device__ __forceinline__ void tiny_xmv_dispatch(TinySmem& S, const KernelDesc& ek, int nu, int m, int lane,
+                                                  const int (&lcol)[kTinySlots], const int (&lrw)[kTinySlots],
+                                                  const int (&lkab)[kTinySlots], const float (&lw)[kTinySlots],
+                                                  const float (&llab)[kTinySlots], int nund, int lr0, int lr1) {
+  switch ((nund + 31) >> 5) {
 #define MGK_TINY_CASE(N) \
-    case N: tiny_xmv<N, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1); break;
+    case N: tiny_xmv<N, EK, LAP>(S, ek, nu, m, lane, lcol, lrw, lkab, lw, llab, nund, lr0, lr1); break;
     MGK_TINY_CASE(1) MGK_TINY_CASE(2) MGK_TINY_CASE(3) MGK_TINY_CASE(4) MGK_TINY_CASE(5)
-    MGK_TINY_CASE(6) MGK_TINY_CASE(7) MGK_TINY_CASE(8) MGK_TINY_CASE(9) MGK_TINY_CASE(10)
 #undef MGK_TINY_CASE
     default:  // edgeless L: OFF = 0 (an edgeless U has no rows to walk either)
       for (int e = lane; e < nu * m; e += 32) S.AP[e] = S.SS[e] * S.P[e];
@@ -247,29 +238,52 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
   const bool vlab = (vk.kind != KK_CONST1 && vk.kind != KK_NONE && ds.nl_kind != LK_NONE);
   // kappa_e = 1 with a large diag / s: A p = s p - sum c (p_j - p_i), s in FP64 (mgk_dev.cuh kLapFactor)
   const bool lap = EK == KK_NONE && laplacian_pair(prm, U, L);
-  // lane slots of L: nonzero k' = lane + 32 t -> column, row, weight, label
-  const int SL = 2 * L.ne, ns = (SL + 31) >> 5;
-  int lcol[kTinySlots], lrw[kTinySlots];
+  // lane slots of L: undirected edge u = lane + 32 t = {l, c} (l < c) -> columns c and l, weight, label and
+  // the directed positions of l -> c and c -> l (upper entries compacted by ballot into SEG first)
+  const int SL = 2 * L.ne, nund = SL >> 1;
+  int lcol[kTinySlots], lrw[kTinySlots], lkab[kTinySlots];
   float lw[kTinySlots], llab[kTinySlots];
   {
     const float4* lr = ds.rowent + L.nz_off;
-#pragma unroll
-    for (int t = 0; t < kTinySlots; ++t) {
-      const int k = lane + 32 * t;
-      lcol[t] = 0;
-      lrw[t] = 0;
-      lw[t] = 0.0f;
-      llab[t] = 0.0f;
+    int* upos = reinterpret_cast<int*>(S.SEG);
+    int base = 0;
+    for (int k0 = 0; k0 < SL; k0 += 32) {
+      const int k = k0 + lane;
+      bool up = false;
       if (k < SL) {
-        const float4 e = lr[k];
-        lcol[t] = __float_as_int(e.x);
-        lw[t] = e.y;
-        llab[t] = e.z;
         int r = 0;
         while (S.lrow[r + 1] <= k) ++r;
-        lrw[t] = r;
+        up = r < __float_as_int(lr[k].x);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, up);
+      if (up) upos[base + __popc(bal & ((1u << lane) - 1u))] = k;
+      base += __popc(bal);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < kTinySlots; ++t) {
+      const int u = lane + 32 * t;
+      lcol[t] = 0;
+      lrw[t] = 0;
+      lkab[t] = 0;
+      lw[t] = 0.0f;
+      llab[t] = 0.0f;
+      if (u < nund) {
+        const int ka = upos[u];
+        const float4 e = lr[ka];
+        int l = 0;
+        while (S.lrow[l + 1] <= ka) ++l;
+        const int c = __float_as_int(e.x);
+        int kb = S.lrow[c];
+        while (__float_as_int(lr[kb].x) != l) ++kb;
+        lcol[t] = c;
+        lrw[t] = l;
+        lw[t] = e.y;
+        llab[t] = e.z;
+        lkab[t] = ka | (kb << 16);
       }
     }
+    __syncwarp();
   }
   const int lr0 = lane < m ? S.lrow[lane] : 0, lr1 = lane < m ? S.lrow[lane + 1] : 0;
   double bb_u = 0.0, bb_l = 0.0;
@@ -309,9 +323,9 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
   __syncwarp();
   while (!conv && it < max_iter) {
     if (lap)
-      tiny_xmv_dispatch<EK, true>(ns, S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1);
+      tiny_xmv_dispatch<EK, true>(S, ek, nu, m, lane, lcol, lrw, lkab, lw, llab, nund, lr0, lr1);
     else
-      tiny_xmv_dispatch<EK, false>(ns, S, ek, nu, m, lane, lcol, lrw, lw, llab, lr0, lr1);
+      tiny_xmv_dispatch<EK, false>(S, ek, nu, m, lane, lcol, lrw, lkab, lw, llab, nund, lr0, lr1);
     ++it;
     double pap = 0.0;
 #pragma unroll
@@ -400,6 +414,89 @@ __device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& 
   }
 }
 
+// acc[t], acc_b[t] += kappa(e_k, e'_t) w_k P[j_k][c_t] and ... P[j_k][l_t]: undirected L edge t = {l_t, c_t}
+// (one edge-kernel value for both directed entries; the per-entry accumulation order is unchanged)
+template <int NSU, int EK, int SLM, class Smem>
+__device__ __forceinline__ void accumulate_row_sym(const Smem& S, const KernelDesc& ek, int i, const char* pbase,
+                                                   const int (&lcoff)[SLM], const int (&lroff)[SLM],
+                                                   const float (&llab)[SLM], float (&acc)[NSU],
+                                                   float (&accb)[NSU]) {
+  const int k1 = S.urow[i + 1];
+  int k = S.urow[i];
+  for (; k + 1 < k1; k += 2) {
+    const float4 e0 = S.UE[k], e1 = S.UE[k + 1];
+    const char* r0 = pbase + __float_as_int(e0.z);
+    const char* r1 = pbase + __float_as_int(e1.z);
+    float pa0[NSU], pb0[NSU], pa1[NSU], pb1[NSU];
+#pragma unroll
+    for (int t = 0; t < NSU; ++t) {
+      pa0[t] = *reinterpret_cast<const float*>(r0 + lcoff[t]);
+      pb0[t] = *reinterpret_cast<const float*>(r0 + lroff[t]);
+      pa1[t] = *reinterpret_cast<const float*>(r1 + lcoff[t]);
+      pb1[t] = *reinterpret_cast<const float*>(r1 + lroff[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < NSU; ++t) {
+      const float c0 = edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x);
+      const float c1 = edge_kappa_w<EK>(ek, e1.y, llab[t], e1.x);
+      acc[t] = fmaf(c0, pa0[t], acc[t]);
+      accb[t] = fmaf(c0, pb0[t], accb[t]);
+      acc[t] = fmaf(c1, pa1[t], acc[t]);
+      accb[t] = fmaf(c1, pb1[t], accb[t]);
+    }
+  }
+  if (k < k1) {
+    const float4 e0 = S.UE[k];
+    const char* r0 = pbase + __float_as_int(e0.z);
+#pragma unroll
+    for (int t = 0; t < NSU; ++t) {
+      const float c0 = edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x);
+      acc[t] = fmaf(c0, *reinterpret_cast<const float*>(r0 + lcoff[t]), acc[t]);
+      accb[t] = fmaf(c0, *reinterpret_cast<const float*>(r0 + lroff[t]), accb[t]);
+    }
+  }
+}
+
+// Labeled XMV over undirected L slots (NSU = ceil(S_L / 64)): each pass accumulates two U rows, writes
+// the slot products to the directed positions of the segment buffer, and sums the L-row segments.
+template <int NSU, int EK, int SLM, class Smem>
+__device__ __forceinline__ void xmv_labeled_sym(Smem& S, const KernelDesc& ek, int nu, int m, int lane,
+                                                const int (&lcoff)[SLM], const int (&lroff)[SLM],
+                                                const int (&lkab)[SLM], const float (&lw)[SLM],
+                                                const float (&llab)[SLM], int lr0, int lr1, int nund) {
+  const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
+  for (int i = 0; i < nu; i += 2) {
+    const bool two = i + 1 < nu;
+    float a0[NSU], b0[NSU], a1[NSU], b1[NSU];
+#pragma unroll
+    for (int t = 0; t < NSU; ++t) a0[t] = b0[t] = a1[t] = b1[t] = 0.0f;
+    accumulate_row_sym<NSU, EK, SLM>(S, ek, i, pbase, lcoff, lroff, llab, a0, b0);
+    if (two) accumulate_row_sym<NSU, EK, SLM>(S, ek, i + 1, pbase, lcoff, lroff, llab, a1, b1);
+#pragma unroll
+    for (int t = 0; t < NSU; ++t) {
+      if (lane + 32 * t < nund) {
+        const int ka = lkab[t] & 0xffff, kb = lkab[t] >> 16;
+        S.SEG[ka] = a0[t] * lw[t];
+        S.SEG[kb] = b0[t] * lw[t];
+        S.SEG[32 * SLM + ka] = a1[t] * lw[t];
+        S.SEG[32 * SLM + kb] = b1[t] * lw[t];
+      }
+    }
+    __syncwarp();
+    if (lane < m) {
+      float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 2
+      for (int q = lr0; q < lr1; ++q) {
+        s0 += S.SEG[q];
+        s1 += S.SEG[32 * SLM + q];
+      }
+      S.OFF[i][lane] = s0;
+      if (two) S.OFF[i + 1][lane] = s1;
+    }
+    __syncwarp();
+  }
+}
+
 // Two U-rows per pass: one SEG round trip and one pair of warp syncs per two
 // rows, and two independent summation chains in the segment reduction.
 template <int NS, int EK, int SLM, class Smem>
@@ -478,19 +575,35 @@ __device__ __forceinline__ void xmv_unlabeled(Smem& S, int nu, int m, int lane, 
 template <int EK, int SLM, class Smem>
 __device__ __forceinline__ void xmv_dispatch(int ns, Smem& S, const KernelDesc& ek, int nu, int m, int lane,
                                              const int (&lcoff)[SLM], const float (&lw)[SLM],
-                                             const float (&llab)[SLM], const int (&lroff)[SLM], int lr0, int lr1,
-                                             bool lap, float lbm) {
+                                             const float (&llab)[SLM], const int (&lroff)[SLM],
+                                             const int (&lkab)[SLM], int nund, int lr0, int lr1, bool lap,
+                                             float lbm) {
+  if constexpr (EK != KK_NONE) {
+    switch ((nund + 31) >> 5) {
+      case 1: xmv_labeled_sym<1, EK, SLM>(S, ek, nu, m, lane, lcoff, lroff, lkab, lw, llab, lr0, lr1, nund); return;
+      case 2: xmv_labeled_sym<2, EK, SLM>(S, ek, nu, m, lane, lcoff, lroff, lkab, lw, llab, lr0, lr1, nund); return;
+      case 3:
+        if constexpr (SLM >= 5) xmv_labeled_sym<3, EK, SLM>(S, ek, nu, m, lane, lcoff, lroff, lkab, lw, llab, lr0, lr1, nund);
+        return;
+      case 4:
+        if constexpr (SLM >= 7) xmv_labeled_sym<4, EK, SLM>(S, ek, nu, m, lane, lcoff, lroff, lkab, lw, llab, lr0, lr1, nund);
+        return;
+      case 5:
+        if constexpr (SLM >= 9) xmv_labeled_sym<5, EK, SLM>(S, ek, nu, m, lane, lcoff, lroff, lkab, lw, llab, lr0, lr1, nund);
+        return;
+      default:  // edgeless lane graph: OFF = 0
+        for (int i = 0; i < nu; ++i) S.OFF[i][lane] = 0.0f;
+        __syncwarp();
+        return;
+    }
+  } else {
 #define MGK_XMV_CASE(N)                                                                  \
   case N:                                                                                \
     if constexpr (N <= SLM) {                                                            \
-      if constexpr (EK == KK_NONE) {                                                     \
-        if (lap)                                                                         \
-          xmv_unlabeled<N, SLM, true>(S, nu, m, lane, lcoff, lw, lroff, lr0, lr1, lbm);  \
-        else                                                                             \
-          xmv_unlabeled<N, SLM, false>(S, nu, m, lane, lcoff, lw, lroff, lr0, lr1, lbm); \
-      } else {                                                                           \
-        xmv_labeled<N, EK, SLM>(S, ek, nu, m, lane, lcoff, lw, llab, lr0, lr1);          \
-      }                                                                                  \
+      if (lap)                                                                           \
+        xmv_unlabeled<N, SLM, true>(S, nu, m, lane, lcoff, lw, lroff, lr0, lr1, lbm);    \
+      else                                                                               \
+        xmv_unlabeled<N, SLM, false>(S, nu, m, lane, lcoff, lw, lroff, lr0, lr1, lbm);   \
     }                                                                                    \
     break;
   switch (ns) {
@@ -509,6 +622,7 @@ __device__ __forceinline__ void xmv_dispatch(int ns, Smem& S, const KernelDesc& 
       __syncwarp();
   }
 #undef MGK_XMV_CASE
+  }
   static_assert(SLOTS == 10 && SLM <= SLOTS, "xmv_dispatch covers 1..10 slots");
 }
 
@@ -573,22 +687,66 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     __syncwarp();
     int lcoff[SLM], lroff[SLM];
     float lw[SLM], llab[SLM];
+    int lkab[SLM];  // labeled: SEG positions of the two directed entries of an undirected L edge (16 + 16 bits)
+    if constexpr (UNLAB) {
 #pragma unroll
-    for (int t = 0; t < SLM; ++t) {
-      const int k = lane + 32 * t;
-      lcoff[t] = 0;
-      lroff[t] = 0;
-      lw[t] = 0.0f;
-      llab[t] = 0.0f;
-      if (k < SL) {
-        const float4 e = stage[k];
-        lcoff[t] = __float_as_int(e.x) * 4;
-        lw[t] = e.y;
-        llab[t] = e.z;
-        if constexpr (UNLAB) {  // L row of the slot (Laplacian splitting)
-          int r = 0;
+      for (int t = 0; t < SLM; ++t) {
+        const int k = lane + 32 * t;
+        lcoff[t] = 0;
+        lroff[t] = 0;
+        lw[t] = 0.0f;
+        llab[t] = 0.0f;
+        lkab[t] = 0;
+        if (k < SL) {
+          const float4 e = stage[k];
+          lcoff[t] = __float_as_int(e.x) * 4;
+          lw[t] = e.y;
+          llab[t] = e.z;
+          int r = 0;  // L row of the slot (Laplacian splitting)
           while (S.lrow[r + 1] <= k) ++r;
           lroff[t] = r * 4;
+        }
+      }
+    } else {
+      // Undirected L edges on the lanes: edge {l, c} (l < c) owns both directed entries l->c and c->l,
+      // whose contributions share one edge-kernel value -- one MUFU.EX2 feeds two accumulators.
+      // Upper entries (l < c) in row order, compacted by ballot: UPOS[u] = directed position.
+      int* upos = reinterpret_cast<int*>(S.SEG);
+      int base = 0;
+      for (int k0 = 0; k0 < SL; k0 += 32) {
+        const int k = k0 + lane;
+        bool up = false;
+        if (k < SL) {
+          int r = 0;
+          while (S.lrow[r + 1] <= k) ++r;
+          up = r < __float_as_int(stage[k].x);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, up);
+        if (up) upos[base + __popc(bal & ((1u << lane) - 1u))] = k;
+        base += __popc(bal);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < SLM; ++t) {
+        const int u = lane + 32 * t;
+        lcoff[t] = 0;
+        lroff[t] = 0;
+        lw[t] = 0.0f;
+        llab[t] = 0.0f;
+        lkab[t] = 0;
+        if (u < (SL >> 1)) {
+          const int ka = upos[u];
+          const float4 e = stage[ka];
+          int l = 0;
+          while (S.lrow[l + 1] <= ka) ++l;
+          const int c = __float_as_int(e.x);
+          int kb = S.lrow[c];  // the reverse entry c -> l in row c
+          while (__float_as_int(stage[kb].x) != l) ++kb;
+          lcoff[t] = c * 4;  // l -> c gathers P[j][c]
+          lroff[t] = l * 4;  // c -> l gathers P[j][l]
+          lw[t] = e.y;
+          llab[t] = e.z;
+          lkab[t] = ka | (kb << 16);
         }
       }
     }
@@ -675,7 +833,7 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
 
     while (!conv && it < max_iter) {
       // ---------------- off-diagonal product OFF = (A (x) A' . ke) P
-      xmv_dispatch<EK, SLM>(ns, S, ek, nu, m, lane, lcoff, lw, llab, lroff, lr0, lr1, lap, lbm);
+      xmv_dispatch<EK, SLM>(ns, S, ek, nu, m, lane, lcoff, lw, llab, lroff, lkab, SL >> 1, lr0, lr1, lap, lbm);
       if (self_pair) {
         // self pair: the exact operator maps symmetric fields to symmetric fields;
         // symmetrising keeps the FP32 Krylov space in that subspace as the FP64
