@@ -302,6 +302,7 @@ struct mgk_ctx {
   DBuf<Octile> d_tiles;
   DBuf<int32_t> d_rowptr, d_panel;
   DBuf<float4> d_rowent;
+  DBuf<int2> d_symk;
   DatasetDev ds{};
   KernelDesc vk{}, ek{};
   // solver buffers
@@ -688,10 +689,16 @@ static int prepare(mgk_ctx* c) {
     k_rows_fill<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(nn, c->d_ngraph.ptr, c->d_graphs.ptr, c->d_tiles.ptr,
                                                               c->d_trow.ptr, c->d_nzw.ptr, c->d_nzlabel.ptr,
                                                               c->ds.el_dim, c->d_rowptr.ptr, c->d_rowent.ptr);
+  CUDA_TRY(c->d_symk.alloc(ne));
+  if (ne > 0)
+    k_sym_fill<<<(unsigned)((ne + 255) / 256), 256, 0, s>>>(ne, c->d_ei.ptr, c->d_ej.ptr, c->d_egraph.ptr,
+                                                             c->d_graphs.ptr, c->d_rowptr.ptr, c->d_rowent.ptr,
+                                                             c->d_symk.ptr);
   CUDA_TRY(cudaGetLastError());
   ds.rowptr = c->d_rowptr.ptr;
   ds.rowent = c->d_rowent.ptr;
   ds.panel_row = c->d_panel.ptr;
+  ds.symk = c->d_symk.ptr;
   c->h_hist.clear();
   c->prepared = true;
   return MGK_OK;

@@ -160,6 +160,8 @@ struct DatasetDev {
   const int32_t* rowptr;       // [sum (n + 1)] relative to the graph's nz base
   const float4* rowent;        // [sum S] {col (int bits), w, label0, 0} ascending column per row
   const int32_t* panel_row;    // [sum (npanels + 1)] first row of every panel
+  const int2* symk;            // [sum E] per undirected edge (i, j): positions of i->j and j->i in the row
+                               // expansion (relative to the graph's nz base; k_sym_fill)
 };
 
 __host__ __device__ inline int ceil8(int n) { return (n + 7) >> 3; }

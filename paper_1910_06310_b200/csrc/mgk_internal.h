@@ -148,6 +148,8 @@ __global__ void k_trow(int, const int64_t*, const int64_t*, GraphDesc*, int32_t*
 __global__ void k_rows_fill(int64_t, const int32_t*, const GraphDesc*, const Octile*, const int32_t*, const float*,
                             const float*, int, const int32_t*, float4*);
 constexpr int kSortSmemBytes = 8192 * 8;
+__global__ void k_sym_fill(int64_t, const int32_t*, const int32_t*, const int32_t*, const GraphDesc*, const int32_t*,
+                           const float4*, int2*);
 constexpr int kHistBins = 66;  // k_tile_hist: tiles per nonzero count 0..64, then non-empty tile rows
 __global__ void k_tile_hist(const GraphDesc*, const Octile*, const int32_t*, int32_t*);
 

@@ -139,7 +139,8 @@ struct PairView {
   const int32_t* lrp;
   const float4* le;
   const int32_t* prow;  // L panel row boundaries (null: single panel = all rows)
-  int n, m, np, rpc;
+  const int2* lsym;     // L's undirected edges: directed positions (i -> j, j -> i) in le (ds.symk)
+  int n, m, np, rpc, nund;
 };
 
 // AP = diag * P - XMV(P) over the (panel, chunk) items w0, w0 + wstride, ...
@@ -265,11 +266,164 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
   }
 }
 
+// Single-panel labeled XMV over undirected L slots: slot t = L edge {l, c}; one edge-kernel evaluation
+// feeds both directed entries (gathers P[j][c] -> lands on row l, P[j][l] -> lands on row c), the slot
+// products go to both directed positions of the segment buffer, and the L-row segment sums are as in
+// xmv_panels (same per-entry accumulation order: results identical to the directed slots).
+template <int NSU, int EK>
+__device__ void xmv_panels_sym(const KernelDesc& ek, const PairView& v, const float* P, float* AP, const float* DG,
+                               float* SEG, int lane, int64_t w0, int64_t wstride, const float* pu, const float* pl,
+                               double2* part) {
+  const int n = v.n, m = v.m;
+  const int nchunks = (n + v.rpc - 1) / v.rpc;
+  int lca[NSU], lcb[NSU], lkab[NSU];
+  float lw[NSU], llab[NSU];
+#pragma unroll
+  for (int t = 0; t < NSU; ++t) {
+    const int u = lane + 32 * t;
+    lca[t] = lcb[t] = lkab[t] = 0;
+    lw[t] = llab[t] = 0.0f;
+    if (u < v.nund) {
+      const int2 kk = v.lsym[u];
+      const float4 e = v.le[kk.x];
+      lca[t] = __float_as_int(e.x);           // l -> c gathers P[j][c]
+      lcb[t] = __float_as_int(v.le[kk.y].x);  // c -> l gathers P[j][l]
+      lw[t] = e.y;
+      llab[t] = e.z;
+      lkab[t] = kk.x | (kk.y << 16);
+    }
+  }
+  const int ra = lane, rb = lane + 32;
+  int qa0 = 0, qa1 = 0, qb0 = 0, qb1 = 0;
+  float pla = 0.0f, plb = 0.0f;
+  if (ra < m) {
+    qa0 = v.lrp[ra];
+    qa1 = v.lrp[ra + 1];
+    if (part) pla = pl[ra];
+  }
+  if (rb < m) {
+    qb0 = v.lrp[rb];
+    qb1 = v.lrp[rb + 1];
+    if (part) plb = pl[rb];
+  }
+  double pap = 0.0, pxp = 0.0;
+  for (int64_t c = w0; c < nchunks; c += wstride) {
+    const int i0 = (int)c * v.rpc, i1 = min(n, i0 + v.rpc);
+    for (int i = i0; i < i1; i += 2) {
+      const bool two = i + 1 < i1;
+      float a[2][NSU], b[2][NSU];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+#pragma unroll
+        for (int t = 0; t < NSU; ++t) a[r][t] = b[r][t] = 0.0f;
+        if (r == 1 && !two) break;
+        const int k1 = v.urp[i + r + 1];
+        int k = v.urp[i + r];
+        for (; k + 1 < k1; k += 2) {
+          const float4 e0 = v.ue[k], e1 = v.ue[k + 1];
+          const float* r0 = P + __float_as_int(e0.x) * m;
+          const float* r1 = P + __float_as_int(e1.x) * m;
+#pragma unroll
+          for (int t = 0; t < NSU; ++t) {
+            const float x0a = r0[lca[t]], x0b = r0[lcb[t]], x1a = r1[lca[t]], x1b = r1[lcb[t]];
+            const float c0 = edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y);
+            const float c1 = edge_kappa_w<EK>(ek, e1.z, llab[t], EK == KK_SE ? e1.w : e1.y);
+            a[r][t] = fmaf(c0, x0a, a[r][t]);
+            b[r][t] = fmaf(c0, x0b, b[r][t]);
+            a[r][t] = fmaf(c1, x1a, a[r][t]);
+            b[r][t] = fmaf(c1, x1b, b[r][t]);
+          }
+        }
+        if (k < k1) {
+          const float4 e0 = v.ue[k];
+          const float* r0 = P + __float_as_int(e0.x) * m;
+#pragma unroll
+          for (int t = 0; t < NSU; ++t) {
+            const float c0 = edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y);
+            a[r][t] = fmaf(c0, r0[lca[t]], a[r][t]);
+            b[r][t] = fmaf(c0, r0[lcb[t]], b[r][t]);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < NSU; ++t) {
+        if (lane + 32 * t < v.nund) {
+          const int ka = lkab[t] & 0xffff, kb = lkab[t] >> 16;
+          SEG[ka] = a[0][t] * lw[t];
+          SEG[kb] = b[0][t] * lw[t];
+          SEG[kPanelCap + ka] = a[1][t] * lw[t];
+          SEG[kPanelCap + kb] = b[1][t] * lw[t];
+        }
+      }
+      __syncwarp();
+      const int base = i * m;
+      float pu0 = 0.0f, pu1 = 0.0f;
+      if (part) {
+        pu0 = pu[i];
+        pu1 = two ? pu[i + 1] : 0.0f;
+      }
+      for (int r = ra; r < m; r += 32) {
+        int q0, q1;
+        float plr;
+        if (r == ra) {
+          q0 = qa0;
+          q1 = qa1;
+          plr = pla;
+        } else if (r == rb) {
+          q0 = qb0;
+          q1 = qb1;
+          plr = plb;
+        } else {
+          q0 = v.lrp[r];
+          q1 = v.lrp[r + 1];
+          plr = part ? pl[r] : 0.0f;
+        }
+        float s0 = 0.0f, s1 = 0.0f;
+        for (int q = q0; q < q1; ++q) {
+          s0 += SEG[q];
+          s1 += SEG[kPanelCap + q];
+        }
+        const int e0 = base + r;
+        const float p0 = P[e0];
+        const float a0 = fmaf(DG[e0], p0, -s0);
+        AP[e0] = a0;
+        if (part) {
+          pap += (double)p0 * (double)a0;
+          pxp += (double)(pu0 * plr) * (double)p0;
+        }
+        if (two) {
+          const float p1 = P[e0 + m];
+          const float a1 = fmaf(DG[e0 + m], p1, -s1);
+          AP[e0 + m] = a1;
+          if (part) {
+            pap += (double)p1 * (double)a1;
+            pxp += (double)(pu1 * plr) * (double)p1;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (part) {
+    part->x += pap;
+    part->y += pxp;
+  }
+}
+
 template <int EK>
 __device__ __forceinline__ void xmv_dispatch(int ns, const KernelDesc& ek, const PairView& v, const float* P,
                                              float* AP, const float* DG, float* SEG, int lane, int64_t w0,
                                              int64_t wstride, const float* pu, const float* pl, double2* part,
                                              bool lap) {
+  if constexpr (EK != KK_NONE) {
+    if (!v.prow && v.nund > 0) {  // single panel (S_L <= 128): undirected slots, one kappa per L edge
+      if (v.nund <= 32)
+        xmv_panels_sym<1, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part);
+      else
+        xmv_panels_sym<2, EK>(ek, v, P, AP, DG, SEG, lane, w0, wstride, pu, pl, part);
+      return;
+    }
+  }
   if constexpr (EK == KK_NONE) {
     if (lap) {
       switch (ns) {
@@ -469,6 +623,8 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     v.lrp = ds.rowptr + L.rowptr_off;
     v.le = ds.rowent + L.nz_off;
     v.prow = SL > 128 ? ds.panel_row + L.panel_off : nullptr;
+    v.lsym = ds.symk + L.edge_off;
+    v.nund = L.ne;
     v.n = n;
     v.m = m;
     v.np = SL > 128 ? L.npanels : 1;
@@ -826,6 +982,8 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     v.lrp = ds.rowptr + L.rowptr_off;
     v.le = ds.rowent + L.nz_off;
     v.prow = SL > 128 ? ds.panel_row + L.panel_off : nullptr;
+    v.lsym = ds.symk + L.edge_off;
+    v.nund = L.ne;
     v.n = n;
     v.m = m;
     v.np = SL > 128 ? L.npanels : 1;

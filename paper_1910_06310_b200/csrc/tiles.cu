@@ -224,6 +224,30 @@ __global__ void k_trow(int G, const int64_t* __restrict__ gseg, const int64_t* _
   graphs[gidx] = g;
 }
 
+// Directed positions of both orientations of every undirected edge in the row expansion (rows
+// ascending, columns ascending within a row): thread per edge, binary search of the two rows.  The
+// solvers pair the two entries of an L edge on one lane (one edge-kernel evaluation for both).
+__device__ __forceinline__ int row_find(const float4* ent, int lo, int hi, int col) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__float_as_int(ent[mid].x) < col) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_sym_fill(int64_t ne, const int32_t* __restrict__ ei, const int32_t* __restrict__ ej,
+                           const int32_t* __restrict__ edge_graph, const GraphDesc* __restrict__ graphs,
+                           const int32_t* __restrict__ rowptr, const float4* __restrict__ rowent,
+                           int2* __restrict__ symk) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const GraphDesc g = graphs[edge_graph[e]];
+  const int i = ei[e], j = ej[e];
+  const int32_t* rp = rowptr + g.rowptr_off;
+  const float4* ent = rowent + g.nz_off;
+  symk[e] = make_int2(row_find(ent, rp[i], rp[i + 1], j), row_find(ent, rp[j], rp[j + 1], i));
+}
+
 // Per-graph octile density histogram for the reference's cost counters (product.py:224-266): hist[g][k] =
 // tiles with k nonzeros (k = 1..64), hist[g][65] = non-empty tile rows.  One CTA per graph.
 __global__ void k_tile_hist(const GraphDesc* __restrict__ graphs, const Octile* __restrict__ tiles,
