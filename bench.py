@@ -252,6 +252,22 @@ def traffic_from_profiles(cfg: Config):
     return None, None
 
 
+def ncu_pipes(cfg: Config):
+    """Pipe utilisation of the dominant kernel from the newest committed ncu --set full summary (config 2's
+    narrow warp solver), or None."""
+    if cfg.key not in ("1", "2"):
+        return None
+    for p in sorted((ROOT / "profiles").glob("*ncu_full_narrow_c2*.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+            return {"source": p.name, **{k.split(".")[0]: v for k, v in d.get("pipes", {}).items()},
+                    "issue_active_pct": d["launches"][0].get("issue_active_pct"),
+                    "ipc_active": d["launches"][0].get("ipc_active")}
+        except Exception:
+            continue
+    return None
+
+
 _PERMS = {}
 
 
@@ -572,6 +588,9 @@ def run_ours(args, rank, world, local_rank):
                                "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
                 "flops_per_launch": flops / world,
                 "flops_convention": f"sum over pairs of I*(X*S_a*S_b + 15*n_a*n_b), X={cfg.x_flops} (SURVEY §8d)",
+                "ex2_convention": "one edge-kernel evaluation per directed contribution (the reference's "
+                                  "formulation); the solvers evaluate one per undirected lane-graph edge, half of it",
+                "ncu_pipes": ncu_pipes(cfg),
                 "ex2_per_launch": exps / world,
                 "ex2_achieved_tops": exps / world / (ms_solve * 1e-3) / 1e12,
                 "ex2_peak_tops": ex2_peak,
