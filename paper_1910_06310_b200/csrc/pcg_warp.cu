@@ -379,41 +379,8 @@ __device__ __forceinline__ void solve_tiny(const DatasetDev& ds, const KernelDes
 }
 
 // ---------------------------------------------------------------------------
-// XMV, labeled: OFF[i][l] for all U-rows i, NS slots per lane.
+// XMV, labeled: OFF[i][l] for all U-rows i, undirected L slots per lane.
 // ---------------------------------------------------------------------------
-// acc[t] += sum_{k in U(i)} kappa(e_k, e'_t) w_k P[j_k][col_L(t)]  (row i of U)
-template <int NS, int EK, int SLM, class Smem>
-__device__ __forceinline__ void accumulate_row(const Smem& S, const KernelDesc& ek, int i, const char* pbase,
-                                               const int (&lcoff)[SLM], const float (&llab)[SLM],
-                                               float (&acc)[NS]) {
-  const int k1 = S.urow[i + 1];
-  int k = S.urow[i];
-  for (; k + 1 < k1; k += 2) {
-    const float4 e0 = S.UE[k], e1 = S.UE[k + 1];
-    const char* r0 = pbase + __float_as_int(e0.z);
-    const char* r1 = pbase + __float_as_int(e1.z);
-    float p0[NS], p1[NS];
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      p0[t] = *reinterpret_cast<const float*>(r0 + lcoff[t]);
-      p1[t] = *reinterpret_cast<const float*>(r1 + lcoff[t]);
-    }
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), p0[t], acc[t]);
-      acc[t] = fmaf(edge_kappa_w<EK>(ek, e1.y, llab[t], e1.x), p1[t], acc[t]);
-    }
-  }
-  if (k < k1) {
-    const float4 e0 = S.UE[k];
-    const char* r0 = pbase + __float_as_int(e0.z);
-#pragma unroll
-    for (int t = 0; t < NS; ++t)
-      acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.y, llab[t], e0.x), *reinterpret_cast<const float*>(r0 + lcoff[t]),
-                    acc[t]);
-  }
-}
-
 // acc[t], acc_b[t] += kappa(e_k, e'_t) w_k P[j_k][c_t] and ... P[j_k][l_t]: undirected L edge t = {l_t, c_t}
 // (one edge-kernel value for both directed entries; the per-entry accumulation order is unchanged)
 template <int NSU, int EK, int SLM, class Smem>
@@ -497,40 +464,7 @@ __device__ __forceinline__ void xmv_labeled_sym(Smem& S, const KernelDesc& ek, i
   }
 }
 
-// Two U-rows per pass: one SEG round trip and one pair of warp syncs per two
-// rows, and two independent summation chains in the segment reduction.
-template <int NS, int EK, int SLM, class Smem>
-__device__ __forceinline__ void xmv_labeled(Smem& S, const KernelDesc& ek, int nu, int m, int lane,
-                                            const int (&lcoff)[SLM], const float (&lw)[SLM],
-                                            const float (&llab)[SLM], int lr0, int lr1) {
-  const char* pbase = reinterpret_cast<const char*>(&S.P[0][0]);
-  for (int i = 0; i < nu; i += 2) {
-    const bool two = i + 1 < nu;
-    float acc0[NS], acc1[NS];
-#pragma unroll
-    for (int t = 0; t < NS; ++t) acc0[t] = acc1[t] = 0.0f;
-    accumulate_row<NS, EK, SLM>(S, ek, i, pbase, lcoff, llab, acc0);
-    if (two) accumulate_row<NS, EK, SLM>(S, ek, i + 1, pbase, lcoff, llab, acc1);
-#pragma unroll
-    for (int t = 0; t < NS; ++t) {
-      S.SEG[lane + 32 * t] = acc0[t] * lw[t];
-      S.SEG[32 * SLM + lane + 32 * t] = acc1[t] * lw[t];
-    }
-    __syncwarp();
-    if (lane < m) {
-      float s0 = 0.0f, s1 = 0.0f;
-#pragma unroll 2
-      for (int q = lr0; q < lr1; ++q) {
-        s0 += S.SEG[q];
-        s1 += S.SEG[32 * SLM + q];
-      }
-      S.OFF[i][lane] = s0;
-      if (two) S.OFF[i + 1][lane] = s1;
-    }
-    __syncwarp();
-  }
-}
-
+// ---------------------------------------------------------------------------
 // XMV, unlabeled (kappa = 1): T = P B^T (slots + segment sums), OFF = A T.
 // LAP (Laplacian splitting, mgk_dev.cuh kLapFactor): OFF = sum L (p_jj' - p_ii') instead, in the same
 // factorised form via p_jj' - p_ii' = (p_jj' - p_ji') + (p_ji' - p_ii'):
