@@ -100,6 +100,11 @@ int mgk_degrees(mgk_ctx* ctx, int32_t g, double* d_out);
  * device-resident benchmark).  max_iter 0 -> 10*n*m (solver.py:87). */
 int mgk_gram(mgk_ctx* ctx, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv);
 
+/* Iteration counts of the last mgk_gram / mgk_gram_normalized on this context as
+ * int64[N*N] (the reference's GramResult.iterations dtype, gram.py:73), widened
+ * on the device so the host receives them without a conversion pass. */
+int mgk_gram_iterations64(mgk_ctx* ctx, int64_t* iters);
+
 /* mgk_gram followed by normalize_gram (gram.py:98-107) on the device-resident
  * matrix: K[a,b] / sqrt(K[a,a] K[b,b]), unit diagonal, NaN propagates; a
  * non-NaN diagonal entry <= 0 fails with MGK_E_INVALID (the reference's

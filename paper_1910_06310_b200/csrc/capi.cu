@@ -1147,6 +1147,18 @@ int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters
   return MGK_OK;
 }
 
+int mgk_gram_iterations64(mgk_ctx* c, int64_t* iters) {
+  if (!c || !iters) return fail(MGK_E_INVALID, "null argument");
+  const int64_t G = c->G;
+  if (c->d_Kit.n < (size_t)(G * G)) return fail(MGK_E_STATE, "no Gram solved on this context");
+  DBuf<int64_t> wide;
+  CUDA_TRY(wide.alloc(G * G));
+  CUDA_TRY(launch_widen_i32(G * G, c->d_Kit.ptr, wide.ptr, c->num_sms, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(d2h(iters, wide.ptr, G * G * sizeof(int64_t)));
+  return MGK_OK;
+}
+
 int mgk_gram_normalized(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters, uint8_t* conv) {
   int rc = mgk_gram(c, tol, max_iter, nullptr, iters, conv);
   if (rc) return rc;

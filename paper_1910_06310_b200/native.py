@@ -46,6 +46,7 @@ SIGNATURES = {
     "mgk_gram_shard_device": (C.c_int, [_P, C.c_int, C.c_int, C.c_double, C.c_int64, _P, _P, _P, _P, _P, _P]),
     "mgk_gram_assemble": (C.c_int, [C.c_int, C.c_int64, _P, _P, _P, _P, _P, C.c_int64, _P, _P, _P]),
     "mgk_gram_multi": (C.c_int, [_P, C.c_int, C.c_double, C.c_int64, _P, _P, _P]),
+    "mgk_gram_iterations64": (C.c_int, [_P, _P]),
 }
 
 
@@ -169,19 +170,21 @@ class Context:
             check(self.lib.mgk_gram(self.h, float(tol), int(max_iter), None, None, None))
             return None
         K = np.empty((G, G), dtype=np.float64)
-        it = np.empty((G, G), dtype=np.int32)
         cv = np.empty((G, G), dtype=np.uint8)
-        check(self.lib.mgk_gram(self.h, float(tol), int(max_iter), _ptr(K), _ptr(it), _ptr(cv)))
-        return K, it, cv.astype(bool)
+        check(self.lib.mgk_gram(self.h, float(tol), int(max_iter), _ptr(K), None, _ptr(cv)))
+        it = np.empty((G, G), dtype=np.int64)  # widened on the device (GramResult.iterations is int64)
+        check(self.lib.mgk_gram_iterations64(self.h, _ptr(it)))
+        return K, it, cv.view(bool)
 
     def gram_normalized(self, tol: float, max_iter: int = 0):
         """Gram matrix normalised on the device (normalize_gram, gram.py:98-107)."""
         G = self.G
         K = np.empty((G, G), dtype=np.float64)
-        it = np.empty((G, G), dtype=np.int32)
         cv = np.empty((G, G), dtype=np.uint8)
-        check(self.lib.mgk_gram_normalized(self.h, float(tol), int(max_iter), _ptr(K), _ptr(it), _ptr(cv)))
-        return K, it, cv.astype(bool)
+        check(self.lib.mgk_gram_normalized(self.h, float(tol), int(max_iter), _ptr(K), None, _ptr(cv)))
+        it = np.empty((G, G), dtype=np.int64)
+        check(self.lib.mgk_gram_iterations64(self.h, _ptr(it)))
+        return K, it, cv.view(bool)
 
     def gram_shard(self, rank: int, world: int, tol: float, max_iter: int = 0):
         """This rank's share of the Gram pairs: (a, b, value, iterations, converged)."""
