@@ -771,6 +771,7 @@ static SolveParams make_params(const mgk_ctx* c, double tol, int64_t max_iter) {
   p.labeled = (c->el_kind != LK_NONE && c->espec.kind != KK_NONE && c->espec.kind != KK_CONST1) ? 1 : 0;
   p.fp64 = (!p.labeled && (tol < kPreciseTol || c->max_dqr > 2.0f * kPreciseLap)) ? 1 : 0;
   if (const char* e = getenv("MGK_FP64")) p.fp64 = atoi(e) ? 1 : 0;
+  p.factor_ratio4 = getenv("MGK_FACTOR_RATIO4") ? std::max(0, atoi(getenv("MGK_FACTOR_RATIO4"))) : 12;
   return p;
 }
 

@@ -58,6 +58,8 @@ struct SolveParams {
   int32_t panel_rpc;        // U rows per panel work item (0: automatic)
   int32_t lap_mode;         // Laplacian splitting (kappa_e = 1 pairs): 0 off, 1 by factor, 2 always
   int32_t fp64;             // every pair on the block solver with FP64 vectors (precise_tol)
+  int32_t factor_ratio4;    // unlabeled panel / grid pairs use the factored A (P B^T) form when the direct
+                            // form costs more than factor_ratio4 / 4 times as many contributions
 };
 
 // kappa_e = 1 systems solved to a relative residual below this bound run every pair with FP64

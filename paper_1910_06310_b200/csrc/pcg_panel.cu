@@ -55,6 +55,27 @@ constexpr int kPanelStaticSmem = (kPW * kSegFloats + kCacheFloats) * 4;
 // shifted diagonal s of the Laplacian splitting).  capi.cu sizes both with kSlabVectors (mgk_internal.h).
 static_assert(kSlabVectors == 7, "slab layout");
 
+// Streaming (evict-first) access to the per-pair vectors that are read / written once per phase (R,
+// the diagonals, X): they should not displace the P vectors whose scattered gathers feed the XMV from
+// L2 (MGK_PANEL_STREAM=0 builds the plain accesses for A/B runs).
+#ifndef MGK_PANEL_STREAM
+#define MGK_PANEL_STREAM 1
+#endif
+__device__ __forceinline__ float ld_stream(const float* p) {
+#if MGK_PANEL_STREAM
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ void st_stream(float* p, float v) {
+#if MGK_PANEL_STREAM
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -241,7 +262,7 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
         }
         const int e0 = base + r;
         const float p0 = P[e0];
-        const float a0 = fmaf(DG[e0], p0, -s0);
+        const float a0 = fmaf(ld_stream(DG + e0), p0, -s0);
         AP[e0] = a0;
         if (part) {
           pap += (double)p0 * (double)a0;
@@ -249,7 +270,7 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
         }
         if (two) {
           const float p1 = P[e0 + m];
-          const float a1 = fmaf(DG[e0 + m], p1, -s1);
+          const float a1 = fmaf(ld_stream(DG + e0 + m), p1, -s1);
           AP[e0 + m] = a1;
           if (part) {
             pap += (double)p1 * (double)a1;
@@ -385,7 +406,7 @@ __device__ void xmv_panels_sym(const KernelDesc& ek, const PairView& v, const fl
         }
         const int e0 = base + r;
         const float p0 = P[e0];
-        const float a0 = fmaf(DG[e0], p0, -s0);
+        const float a0 = fmaf(ld_stream(DG + e0), p0, -s0);
         AP[e0] = a0;
         if (part) {
           pap += (double)p0 * (double)a0;
@@ -393,7 +414,7 @@ __device__ void xmv_panels_sym(const KernelDesc& ek, const PairView& v, const fl
         }
         if (two) {
           const float p1 = P[e0 + m];
-          const float a1 = fmaf(DG[e0 + m], p1, -s1);
+          const float a1 = fmaf(ld_stream(DG + e0 + m), p1, -s1);
           AP[e0 + m] = a1;
           if (part) {
             pap += (double)p1 * (double)a1;
@@ -553,7 +574,7 @@ __device__ void factored_AP(const PairView& v, const float* P, const float* T, f
       }
     }
     const float p = P[e];
-    const float ap = fmaf(DG[e], p, -acc);
+    const float ap = fmaf(ld_stream(DG + e), p, -acc);
     AP[e] = ap;
     if (part) {
       pap += (double)p * (double)ap;
@@ -724,7 +745,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     double value = 0.0;
     const bool self_pair = (ga == gb);
     // unlabeled: factorise when it saves work beyond its extra pass (not for degree-4 sparsity)
-    const bool factor = (int64_t)(2 * U.ne) * SL > 3 * ((int64_t)n * SL + (int64_t)(2 * U.ne) * m);
+    const bool factor = (int64_t)(2 * U.ne) * SL * 4 > prm.factor_ratio4 * ((int64_t)n * SL + (int64_t)(2 * U.ne) * m);
     __syncthreads();
 
     while (!conv && it < max_iter) {
@@ -776,10 +797,10 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
       // pass 2: x += alpha p, r -= alpha Ap, z = r / diag (stored over Ap)
       acc = make_double2(0.0, 0.0);
       for (int e = threadIdx.x; e < nm; e += kPT) {
-        if constexpr (NODEWISE) X[e] = fmaf(af, P[e], X[e]);
-        const float r = fmaf(-af, AP[e], R[e]);
-        const float z = r * rcp_approx(DG[e]);
-        R[e] = r;
+        if constexpr (NODEWISE) st_stream(X + e, fmaf(af, P[e], ld_stream(X + e)));
+        const float r = fmaf(-af, AP[e], ld_stream(R + e));
+        const float z = r * rcp_approx(ld_stream(DG + e));
+        st_stream(R + e, r);
         AP[e] = z;
         acc.x += (double)r * (double)r;
         acc.y += (double)r * (double)z;
@@ -1036,7 +1057,7 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     int64_t it = 0;
     double value = 0.0;
     const bool self_pair = (ga == gb);
-    const bool factor = (int64_t)(2 * U.ne) * SL > 3 * ((int64_t)n * SL + (int64_t)(2 * U.ne) * m);
+    const bool factor = (int64_t)(2 * U.ne) * SL * 4 > prm.factor_ratio4 * ((int64_t)n * SL + (int64_t)(2 * U.ne) * m);
 
     while (!conv && it < max_iter) {
       double2 part = make_double2(0.0, 0.0);
@@ -1082,10 +1103,10 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       const float af = (float)alpha;
       acc = make_double2(0.0, 0.0);
       for (int64_t e = gtid; e < nm; e += gthreads) {
-        if constexpr (NODEWISE) X[e] = fmaf(af, P[e], X[e]);
-        const float r = fmaf(-af, AP[e], R[e]);
-        const float z = r * rcp_approx(DG[e]);
-        R[e] = r;
+        if constexpr (NODEWISE) st_stream(X + e, fmaf(af, P[e], ld_stream(X + e)));
+        const float r = fmaf(-af, AP[e], ld_stream(R + e));
+        const float z = r * rcp_approx(ld_stream(DG + e));
+        st_stream(R + e, r);
         AP[e] = z;
         acc.x += (double)r * (double)r;
         acc.y += (double)r * (double)z;
