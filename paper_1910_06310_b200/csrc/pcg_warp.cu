@@ -590,8 +590,15 @@ k_pcg_warp(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
     // orientation: L takes the graph that minimises S_U * ceil(S_L / 32), within SLM slots
     const int SA = 2 * A.ne, SB = 2 * B.ne;
     const int nsA = (SA + 31) >> 5, nsB = (SB + 31) >> 5;
-    const long costAB = (long)SA * nsB + A.n;  // U = A, L = B
-    const long costBA = (long)SB * nsA + B.n;
+#ifndef MGK_ORIENT
+#define MGK_ORIENT 0
+#endif
+    // MGK_ORIENT 1 (labeled, undirected slots): shared-memory wavefronts per U nonzero ~ 2 (row entry)
+    // + 2 ceil(S_L / 64) (two gathers per undirected slot)
+    const long costAB = (MGK_ORIENT && EK != KK_NONE) ? (long)SA * (2 + 2 * ((SB + 63) >> 6)) + 4 * A.n
+                                                       : (long)SA * nsB + A.n;  // U = A, L = B
+    const long costBA = (MGK_ORIENT && EK != KK_NONE) ? (long)SB * (2 + 2 * ((SA + 63) >> 6)) + 4 * B.n
+                                                       : (long)SB * nsA + B.n;
     bool swap = (costBA < costAB);
     if (SLM < SLOTS) {
       if ((swap ? nsA : nsB) > SLM) swap = !swap;
