@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <set>
 #include <thread>
@@ -826,9 +827,16 @@ static int64_t block_slab(const mgk_ctx* c, int64_t n, int64_t m, int64_t su, in
 
 // Enqueue every job of `jobs` (device time bracketed by e0 / e1, default the context's events); with
 // sync the call waits for completion and stores the elapsed time in last_ms.
+// Kernel attributes (max dynamic shared memory) are process-wide per function while the panel CTAs'
+// dynamic size varies per job: contexts driven from several host threads (mgk_gram_multi) must not
+// interleave one thread's attribute update with another's launch.
+static std::mutex g_launch_mu;
+
 static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_base,
                     const std::vector<int64_t>& out_offsets, const SolveParams& prm, bool sync = true,
                     cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr) {
+  std::unique_lock<std::mutex> launch_lock(g_launch_mu);
+  CUDA_TRY(cudaSetDevice(c->device));  // the calling thread may have last used another context's device
   cudaStream_t s = c->stream;
   if (!e0) e0 = c->ev0;
   if (!e1) e1 = c->ev1;
@@ -941,6 +949,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
     CUDA_TRY(cudaStreamWaitEvent(s, c->evside[q], 0));
   }
   CUDA_TRY(cudaEventRecord(e1, s));
+  launch_lock.unlock();  // everything is enqueued
   if (!sync) return MGK_OK;
   CUDA_TRY(cudaEventSynchronize(e1));
   CUDA_TRY(cudaGetLastError());

@@ -48,17 +48,29 @@ def tile_graph(rng, R, k, labeled):
 
 
 def main():
-    out = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "profiles" / "r02_density_sweep.json"
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("out", nargs="?", default=str(ROOT / "profiles" / "r02_density_sweep.json"))
+    ap.add_argument("--ks", default="1,2,4,8,16,32,48,64")
+    ap.add_argument("--classes", default="warp,panel")
+    ap.add_argument("--modes", default="labeled,unlabeled")
+    args = ap.parse_args()
+    out = Path(args.out)
     ctx = native.Context(0)
     fp32, ex2 = ctx.peaks(0)
-    ks = [1, 2, 4, 8, 16, 32, 48, 64]
+    ks = [int(k) for k in args.ks.split(",")]
     th = {"labeled": mgk.SelectionThresholds.for_mode("labeled"),
           "unlabeled": mgk.SelectionThresholds.for_mode("unlabeled")}
     cells = []
     # enough pairs per cell to fill the device: 64 x 64 = 4096 warp-class pairs (2368 resident warps),
     # 32 x 32 = 1024 panel-class pairs (~3.5 waves of 296 CTAs)
     for cls, R, per in (("warp", 3, 64), ("panel", 16, 32)):
+        if cls not in args.classes.split(","):
+            continue
         for labeled in (True, False):
+            if ("labeled" if labeled else "unlabeled") not in args.modes.split(","):
+                continue
             mode = "labeled" if labeled else "unlabeled"
             X = 7 if labeled else 3
             vs, es = ("delta:0.5", "se:1.0") if labeled else (None, None)
