@@ -103,6 +103,28 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
                                                const float (&llab)[NS], float (&acc)[NS],
                                                const float (&pc)[NS]) {
   int k = k0;
+#ifndef MGK_PANEL_UNROLL4
+#define MGK_PANEL_UNROLL4 1
+#endif
+  if constexpr (MGK_PANEL_UNROLL4 != 0) {  // four nonzeros per step: 4 NS gathers in flight per warp
+    for (; k + 3 < k1; k += 4) {
+      float4 e[4];
+      float pv[4][NS];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) e[u] = ue[k + u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float* r = P + __float_as_int(e[u].x) * m;
+#pragma unroll
+        for (int t = 0; t < NS; ++t) pv[u][t] = LAP ? r[lcol[t]] - pc[t] : r[lcol[t]];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int t = 0; t < NS; ++t)
+          acc[t] = fmaf(edge_kappa_w<EK>(ek, e[u].z, llab[t], EK == KK_SE ? e[u].w : e[u].y), pv[u][t], acc[t]);
+    }
+  }
   for (; k + 1 < k1; k += 2) {
     const float4 e0 = ue[k], e1 = ue[k + 1];
     const float* r0 = P + __float_as_int(e0.x) * m;
