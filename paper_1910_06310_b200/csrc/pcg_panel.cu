@@ -76,6 +76,74 @@ __device__ __forceinline__ void st_stream(float* p, float v) {
 #endif
 }
 
+// PCG vector passes over the elements e0, e0 + es, ... (es = the CTA's / grid's thread count), four
+// elements per step with every load issued before the arithmetic (the streamed vectors come from
+// HBM: four independent loads in flight per thread instead of one); per-thread accumulation order unchanged.
+// A/B on the box: 4 for the 512-thread panel CTAs and the grid solver (config 3 +1.6 %, config-4 buckets
+// +5-7 %); 1 for the 256-thread CTAs (the extra registers spill there: config 5 -7 % at 4).
+#ifndef MGK_VEC_UNROLL
+#define MGK_VEC_UNROLL (MGK_PANEL_THREADS >= 512 ? 4 : 1)
+#endif
+// x += alpha p, r -= alpha Ap, z = r / diag (stored over Ap); returns (r.r, r.z) partials
+template <bool NODEWISE, class I>
+__device__ __forceinline__ double2 pcg_pass2(I e0, I es, I nm, float af, const float* P, float* AP, float* R,
+                                             const float* DG, float* X) {
+  constexpr int U = MGK_VEC_UNROLL;
+  double2 acc = make_double2(0.0, 0.0);
+  for (I eb = e0; eb < nm; eb += U * es) {
+    float ap[U], rv[U], dg[U], xv[U], pv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const I e = eb + u * es;
+      if (e < nm) {
+        ap[u] = AP[e];
+        rv[u] = ld_stream(R + e);
+        dg[u] = ld_stream(DG + e);
+        if constexpr (NODEWISE) {
+          xv[u] = ld_stream(X + e);
+          pv[u] = P[e];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const I e = eb + u * es;
+      if (e < nm) {
+        if constexpr (NODEWISE) st_stream(X + e, fmaf(af, pv[u], xv[u]));
+        const float r = fmaf(-af, ap[u], rv[u]);
+        const float z = r * rcp_approx(dg[u]);
+        st_stream(R + e, r);
+        AP[e] = z;
+        acc.x += (double)r * (double)r;
+        acc.y += (double)r * (double)z;
+      }
+    }
+  }
+  return acc;
+}
+
+// p = z + beta p (z stored over Ap)
+template <class I>
+__device__ __forceinline__ void pcg_update_p(I e0, I es, I nm, float beta, float* P, const float* AP) {
+  constexpr int U = MGK_VEC_UNROLL;
+  for (I eb = e0; eb < nm; eb += U * es) {
+    float pv[U], zv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const I e = eb + u * es;
+      if (e < nm) {
+        pv[u] = P[e];
+        zv[u] = AP[e];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const I e = eb + u * es;
+      if (e < nm) P[e] = fmaf(beta, pv[u], zv[u]);
+    }
+  }
+}
+
 __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -186,6 +254,28 @@ struct PairView {
   int n, m, np, rpc, nund;
 };
 
+// Largest U-row chunk of a panel-solver item (A/B on config 3 with chunk-major items: 8 rows +5 % over 32)
+#ifndef MGK_PANEL_RPC_MAX
+#define MGK_PANEL_RPC_MAX 8
+#endif
+constexpr int kPanelRpcMax = MGK_PANEL_RPC_MAX;
+
+// Item order: chunk-major (consecutive warps take the panels of one U-row chunk, so the CTA's gathers
+// share the P rows of that chunk's neighbourhood in L1; A/B on the box: +16 % on config 3, +22 % on the
+// SE grid buckets of config 4) or panel-major (MGK_PANEL_CMAJOR=0).
+#ifndef MGK_PANEL_CMAJOR
+#define MGK_PANEL_CMAJOR 1
+#endif
+__device__ __forceinline__ void item_coords(int64_t item, int np, int nchunks, int& p, int& c) {
+#if MGK_PANEL_CMAJOR
+  c = (int)(item / np);
+  p = (int)(item - (int64_t)c * np);
+#else
+  p = (int)(item / nchunks);
+  c = (int)(item - (int64_t)p * nchunks);
+#endif
+}
+
 // AP = diag * P - XMV(P) over the (panel, chunk) items w0, w0 + wstride, ...
 // When part != nullptr the warp also accumulates (p.Ap, px.p) over the
 // elements it wrote (every element is written by exactly one item).
@@ -199,7 +289,8 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
   const int64_t items = (int64_t)v.np * nchunks;
   double pap = 0.0, pxp = 0.0;
   for (int64_t item = w0; item < items; item += wstride) {
-    const int p = (int)(item / nchunks), c = (int)(item - (int64_t)p * nchunks);
+    int p, c;
+    item_coords(item, v.np, nchunks, p, c);
     const int rbeg = v.prow ? v.prow[p] : 0;
     const int rend = v.prow ? v.prow[p + 1] : m;
     const int kbeg = v.lrp[rbeg], kend = v.lrp[rend];
@@ -499,7 +590,8 @@ __device__ void factored_T(const PairView& v, const float* P, float* T, float* S
   const int nchunks = (n + v.rpc - 1) / v.rpc;
   const int64_t items = (int64_t)v.np * nchunks;
   for (int64_t item = w0; item < items; item += wstride) {
-    const int p = (int)(item / nchunks), c = (int)(item - (int64_t)p * nchunks);
+    int p, c;
+    item_coords(item, v.np, nchunks, p, c);
     const int rbeg = v.prow ? v.prow[p] : 0;
     const int rend = v.prow ? v.prow[p + 1] : m;
     const int kbeg = v.lrp[rbeg], kend = v.lrp[rend];
@@ -673,7 +765,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
     v.np = SL > 128 ? L.npanels : 1;
     {
       int rpc = (n * v.np) / (4 * kPW);
-      rpc = rpc < 2 ? 2 : (rpc > 32 ? 32 : rpc);
+      rpc = rpc < 2 ? 2 : (rpc > kPanelRpcMax ? kPanelRpcMax : rpc);
       if (prm.panel_rpc > 0) rpc = prm.panel_rpc;
       v.rpc = (rpc + 1) & ~1;
     }
@@ -817,16 +909,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
       value += alpha * s.y;
       const float af = (float)alpha;
       // pass 2: x += alpha p, r -= alpha Ap, z = r / diag (stored over Ap)
-      acc = make_double2(0.0, 0.0);
-      for (int e = threadIdx.x; e < nm; e += kPT) {
-        if constexpr (NODEWISE) st_stream(X + e, fmaf(af, P[e], ld_stream(X + e)));
-        const float r = fmaf(-af, AP[e], ld_stream(R + e));
-        const float z = r * rcp_approx(ld_stream(DG + e));
-        st_stream(R + e, r);
-        AP[e] = z;
-        acc.x += (double)r * (double)r;
-        acc.y += (double)r * (double)z;
-      }
+      acc = pcg_pass2<NODEWISE, int>((int)threadIdx.x, kPT, nm, af, P, AP, R, DG, X);
       s = block_sum2(acc, red[flip]);
       flip ^= 1;
       rr = s.x;
@@ -836,7 +919,7 @@ k_pcg_panel(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParam
         break;
       }
       const float beta = (float)(rho_next / rho);
-      for (int e = threadIdx.x; e < nm; e += kPT) P[e] = fmaf(beta, P[e], AP[e]);
+      pcg_update_p<int>((int)threadIdx.x, kPT, nm, beta, P, AP);
       rho = rho_next;
       __syncthreads();
     }
@@ -1123,16 +1206,7 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
       const double alpha = rho / s.x;
       value += alpha * s.y;
       const float af = (float)alpha;
-      acc = make_double2(0.0, 0.0);
-      for (int64_t e = gtid; e < nm; e += gthreads) {
-        if constexpr (NODEWISE) st_stream(X + e, fmaf(af, P[e], ld_stream(X + e)));
-        const float r = fmaf(-af, AP[e], ld_stream(R + e));
-        const float z = r * rcp_approx(ld_stream(DG + e));
-        st_stream(R + e, r);
-        AP[e] = z;
-        acc.x += (double)r * (double)r;
-        acc.y += (double)r * (double)z;
-      }
+      acc = pcg_pass2<NODEWISE, int64_t>(gtid, gthreads, (int64_t)nm, af, P, AP, R, DG, X);
       s = gsum(acc);
       rr = s.x;
       const double rho_next = s.y;
@@ -1141,7 +1215,7 @@ k_pcg_grid(DatasetDev ds, KernelDesc vk, KernelDesc ek, PairJob job, SolveParams
         break;
       }
       const float beta = (float)(rho_next / rho);
-      for (int64_t e = gtid; e < nm; e += gthreads) P[e] = fmaf(beta, P[e], AP[e]);
+      pcg_update_p<int64_t>(gtid, gthreads, (int64_t)nm, beta, P, AP);
       rho = rho_next;
       grid.sync();
     }
