@@ -260,9 +260,17 @@ def ncu_pipes(cfg: Config):
     for p in sorted((ROOT / "profiles").glob("*ncu_full_narrow_c2*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
-            return {"source": p.name, **{k.split(".")[0]: v for k, v in d.get("pipes", {}).items()},
-                    "issue_active_pct": d["launches"][0].get("issue_active_pct"),
-                    "ipc_active": d["launches"][0].get("ipc_active")}
+            pipes = {k.split(".")[0]: v for k, v in d.get("pipes", {}).items()}
+            out = {"source": p.name, **pipes, "issue_active_pct": d["launches"][0].get("issue_active_pct"),
+                   "ipc_active": d["launches"][0].get("ipc_active")}
+            # the resource the kernel is bound by: the busiest pipe of the ncu capture (the FP32 fraction
+            # above is the reference's flop convention, not what saturates first)
+            if pipes:
+                k = max(pipes, key=lambda q: pipes[q])
+                out["binding"] = {"pipe": k, "pct_of_peak": pipes[k],
+                                  "note": "shared-memory data-pipe wavefronts (P gathers, row entries, segment "
+                                          "sums)" if "shared" in k else k}
+            return out
         except Exception:
             continue
     return None
