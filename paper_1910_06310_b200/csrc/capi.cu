@@ -869,6 +869,7 @@ static int run_jobs(mgk_ctx* c, std::vector<JobSpec>& jobs, const SolveOut& out_
       int per_sm = big[k] ? p512::panel_ctas_per_sm(0) : p256::panel_ctas_per_sm(svec[k]);
       if (const char* e = getenv("MGK_PANEL_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
       ctas[k] = per_sm * c->num_sms;
+      if (const char* e = getenv("MGK_PANEL_MAX_CTAS")) ctas[k] = std::max(1, std::min(ctas[k], atoi(e)));
     } else {
       continue;
     }
