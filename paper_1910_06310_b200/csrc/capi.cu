@@ -33,6 +33,85 @@ cudaError_t d2h(void* dst, const void* src, size_t bytes) {
   return cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
 }
 
+// Large device -> host result copies (the N x N Gram outputs: ~0.7 GB for config 2) into pageable caller
+// memory: a plain cudaMemcpy stages through the driver's small bounce buffer and first-touches every
+// destination page on one thread.  Here chunks go to two pinned buffers (per host thread) with
+// cudaMemcpyAsync while host threads move the previous chunk into the destination (page faults in
+// parallel); widen = true converts int32 elements to int64 on the way (the Gram iteration counts, whose
+// int64 form the result type needs, cross PCIe at half the size).  The source must be complete
+// (callers synchronise their solve first).
+constexpr size_t kStageBytes = size_t(32) << 20;
+constexpr size_t kStageMin = size_t(64) << 20;
+
+struct Stage {
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  int device = -1;
+};
+thread_local Stage g_stage;
+
+static void host_move(char* dst, const char* src, size_t bytes, bool widen, int threads) {
+  const size_t unit = widen ? 4 : 1;
+  const size_t n = bytes / unit;
+  auto part = [&](int t) {
+    const size_t a = n * t / threads, b = n * (t + 1) / threads;
+    if (widen) {
+      const int32_t* s = reinterpret_cast<const int32_t*>(src);
+      int64_t* d = reinterpret_cast<int64_t*>(dst);
+      for (size_t i = a; i < b; ++i) d[i] = s[i];
+    } else {
+      std::memcpy(dst + a, src + a, b - a);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(part, t);
+  part(0);
+  for (auto& th : pool) th.join();
+}
+
+cudaError_t d2h_staged(void* dst, const void* src, size_t bytes, bool widen = false) {
+  if (bytes < kStageMin && !widen) return d2h(dst, src, bytes);
+  g_d2h_bytes += (int64_t)bytes;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  Stage& S = g_stage;
+  if (S.device != dev) {
+    for (int b = 0; b < 2; ++b) {
+      if (!S.buf[b]) {
+        e = cudaHostAlloc(&S.buf[b], kStageBytes, cudaHostAllocPortable);
+        if (e != cudaSuccess) return e;
+      }
+      if (S.ev[b]) cudaEventDestroy(S.ev[b]);
+      e = cudaEventCreateWithFlags(&S.ev[b], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    if (S.st) cudaStreamDestroy(S.st);
+    e = cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    S.device = dev;
+  }
+  const int threads = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const size_t nchunks = (bytes + kStageBytes - 1) / kStageBytes;
+  auto issue = [&](size_t k) {
+    const size_t off = k * kStageBytes, len = std::min(kStageBytes, bytes - off);
+    cudaError_t r = cudaMemcpyAsync(S.buf[k & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                    S.st);
+    if (r == cudaSuccess) r = cudaEventRecord(S.ev[k & 1], S.st);
+    return r;
+  };
+  if ((e = issue(0)) != cudaSuccess) return e;
+  for (size_t k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks && (e = issue(k + 1)) != cudaSuccess) return e;
+    if ((e = cudaEventSynchronize(S.ev[k & 1])) != cudaSuccess) return e;
+    const size_t off = k * kStageBytes, len = std::min(kStageBytes, bytes - off);
+    host_move(static_cast<char*>(dst) + (widen ? 2 * off : off), static_cast<const char*>(S.buf[k & 1]), len, widen,
+              threads);
+  }
+  return cudaSuccess;
+}
+
 int fail(int code, const char* fmt, ...) {
   char buf[4096];
   va_list ap;
@@ -1152,9 +1231,9 @@ int mgk_gram(mgk_ctx* c, double tol, int64_t max_iter, double* K, int32_t* iters
   std::vector<int64_t> offs(jobs.size(), 0);
   rc = run_jobs(c, jobs, o, offs, prm);
   if (rc) return rc;
-  if (K) CUDA_TRY(d2h(K, c->d_K.ptr, G * G * sizeof(double)));
-  if (iters) CUDA_TRY(d2h(iters, c->d_Kit.ptr, G * G * sizeof(int32_t)));
-  if (conv) CUDA_TRY(d2h(conv, c->d_Kconv.ptr, G * G));
+  if (K) CUDA_TRY(d2h_staged(K, c->d_K.ptr, G * G * sizeof(double)));
+  if (iters) CUDA_TRY(d2h_staged(iters, c->d_Kit.ptr, G * G * sizeof(int32_t)));
+  if (conv) CUDA_TRY(d2h_staged(conv, c->d_Kconv.ptr, G * G));
   return MGK_OK;
 }
 
@@ -1162,11 +1241,10 @@ int mgk_gram_iterations64(mgk_ctx* c, int64_t* iters) {
   if (!c || !iters) return fail(MGK_E_INVALID, "null argument");
   const int64_t G = c->G;
   if (c->d_Kit.n < (size_t)(G * G)) return fail(MGK_E_STATE, "no Gram solved on this context");
-  DBuf<int64_t> wide;
-  CUDA_TRY(wide.alloc(G * G));
-  CUDA_TRY(launch_widen_i32(G * G, c->d_Kit.ptr, wide.ptr, c->num_sms, c->stream));
+  CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(d2h(iters, wide.ptr, G * G * sizeof(int64_t)));
+  // int32 counts cross PCIe and are widened by the host threads that move the staged chunks
+  CUDA_TRY(d2h_staged(iters, c->d_Kit.ptr, G * G * sizeof(int32_t), true));
   return MGK_OK;
 }
 
@@ -1182,7 +1260,7 @@ int mgk_gram_normalized(mgk_ctx* c, double tol, int64_t max_iter, double* K, int
   CUDA_TRY(launch_gram_normalize(c->d_K.ptr, G, diag.ptr, bad.ptr, c->num_sms, c->stream, &nonpositive));
   if (nonpositive) return fail(MGK_E_INVALID, "Gram diagonal must be strictly positive");
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  if (K) CUDA_TRY(d2h(K, c->d_K.ptr, G * G * sizeof(double)));
+  if (K) CUDA_TRY(d2h_staged(K, c->d_K.ptr, G * G * sizeof(double)));
   return MGK_OK;
 }
 

@@ -67,15 +67,4 @@ cudaError_t launch_gram_assemble(int64_t npairs, const int32_t* pa, const int32_
   return cudaGetLastError();
 }
 
-__global__ void k_widen_i32(int64_t n, const int32_t* __restrict__ src, int64_t* __restrict__ dst) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-    dst[k] = src[k];
-}
-
-cudaError_t launch_widen_i32(int64_t n, const int32_t* src, int64_t* dst, int num_sms, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
-  k_widen_i32<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms * 16), 256, 0, stream>>>(n, src, dst);
-  return cudaGetLastError();
-}
-
 }  // namespace mgk

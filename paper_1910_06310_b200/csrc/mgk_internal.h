@@ -194,7 +194,6 @@ MGK_PANEL_DECLS
 // Gram post-processing (gram_post.cu)
 cudaError_t launch_gram_normalize(double* K, int64_t G, double* diag, int* bad, int num_sms, cudaStream_t stream,
                                   bool* nonpositive);
-cudaError_t launch_widen_i32(int64_t n, const int32_t* src, int64_t* dst, int num_sms, cudaStream_t stream);
 cudaError_t launch_gram_assemble(int64_t npairs, const int32_t* pa, const int32_t* pb, const double* value,
                                  const int32_t* iters, const uint8_t* conv, int64_t G, double* K, int32_t* K_iters,
                                  uint8_t* K_conv, int num_sms, cudaStream_t stream);

@@ -162,12 +162,28 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* buf) {
   return s;
 }
 
+// Gather addressing: each lane keeps a pointer to P[0][col(t)] per slot (made opaque to the compiler, so
+// it is not re-associated into (j m + col) << 2 + P with a sign extension and a 64-bit carry chain), and a
+// gather P[j][col(t)] is one IMAD.WIDE.U32 (lane pointer + 4 j m) + the load.  MGK_PANEL_LP=0: P + j m + col.
+#ifndef MGK_PANEL_LP
+#define MGK_PANEL_LP 1
+#endif
+__device__ __forceinline__ const float* opaque_ptr(const float* p) {
+#if MGK_PANEL_LP
+  const float* r;
+  asm("mov.b64 %0, %1;" : "=l"(r) : "l"(p));
+  return r;
+#else
+  return p;
+#endif
+}
+
 // acc[t] += sum_{k in [k0, k1)} kappa(e_k, e'_t) w_k P[j_k][lcol[t]]   (U row, warp-uniform)
 // LAP (kappa_e = 1, Laplacian splitting): the gathered values enter as differences P[j_k][lcol[t]] - pc[t]
 // with pc[t] = P[i][row(t)] the element the contribution lands on (mgk_dev.cuh kLapFactor).
 template <int NS, int EK, bool LAP = false>
 __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float4* __restrict__ ue, int k0, int k1,
-                                               const float* P, int m, const int (&lcol)[NS],
+                                               const float* const (&lp)[NS], int m,
                                                const float (&llab)[NS], float (&acc)[NS],
                                                const float (&pc)[NS]) {
   int k = k0;
@@ -182,9 +198,9 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
       for (int u = 0; u < 4; ++u) e[u] = ue[k + u];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float* r = P + __float_as_int(e[u].x) * m;
+        const unsigned off = (unsigned)(__float_as_int(e[u].x) * m);
 #pragma unroll
-        for (int t = 0; t < NS; ++t) pv[u][t] = LAP ? r[lcol[t]] - pc[t] : r[lcol[t]];
+        for (int t = 0; t < NS; ++t) pv[u][t] = LAP ? lp[t][off] - pc[t] : lp[t][off];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -195,13 +211,12 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
   }
   for (; k + 1 < k1; k += 2) {
     const float4 e0 = ue[k], e1 = ue[k + 1];
-    const float* r0 = P + __float_as_int(e0.x) * m;
-    const float* r1 = P + __float_as_int(e1.x) * m;
+    const unsigned o0 = (unsigned)(__float_as_int(e0.x) * m), o1 = (unsigned)(__float_as_int(e1.x) * m);
     float p0[NS], p1[NS];
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
-      p0[t] = r0[lcol[t]];
-      p1[t] = r1[lcol[t]];
+      p0[t] = lp[t][o0];
+      p1[t] = lp[t][o1];
       if constexpr (LAP) {
         p0[t] -= pc[t];
         p1[t] -= pc[t];
@@ -215,11 +230,11 @@ __device__ __forceinline__ void row_accumulate(const KernelDesc& ek, const float
   }
   if (k < k1) {
     const float4 e0 = ue[k];
-    const float* r0 = P + __float_as_int(e0.x) * m;
+    const unsigned o0 = (unsigned)(__float_as_int(e0.x) * m);
 #pragma unroll
     for (int t = 0; t < NS; ++t)
       acc[t] = fmaf(edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y),
-                    LAP ? r0[lcol[t]] - pc[t] : r0[lcol[t]], acc[t]);
+                    LAP ? lp[t][o0] - pc[t] : lp[t][o0], acc[t]);
   }
 }
 
@@ -259,6 +274,12 @@ struct PairView {
 #define MGK_PANEL_RPC_MAX 8
 #endif
 constexpr int kPanelRpcMax = MGK_PANEL_RPC_MAX;
+
+// Prefetch of the epilogue diagonal (A/B on the box: config 3 +3 % on the 512-thread CTAs; config 5's
+// 256-thread CTAs -1.4 %, so off there)
+#ifndef MGK_PANEL_DGPF
+#define MGK_PANEL_DGPF (MGK_PANEL_THREADS >= 512)
+#endif
 
 // Item order: chunk-major (consecutive warps take the panels of one U-row chunk, so the CTA's gathers
 // share the P rows of that chunk's neighbourhood in L1; A/B on the box: +16 % on config 3, +22 % on the
@@ -311,6 +332,9 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
     }
     int lrw[NS];
     if constexpr (LAP) slot_rows<NS>(v.lrp, rbeg, rend, kbeg, kend, lane, lrw);
+    const float* lp[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) lp[t] = opaque_ptr(P + lcol[t]);
     // this lane's first two panel rows, cached
     const int ra = rbeg + lane, rb = rbeg + lane + 32;
     int qa0 = 0, qa1 = 0, qb0 = 0, qb1 = 0;
@@ -338,8 +362,17 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
           if (two) pc1[t] = P[(i + 1) * m + lrw[t]];
         }
       }
-      row_accumulate<NS, EK, LAP>(ek, v.ue, v.urp[i], v.urp[i + 1], P, m, lcol, llab, acc0, pc0);
-      if (two) row_accumulate<NS, EK, LAP>(ek, v.ue, v.urp[i + 1], v.urp[i + 2], P, m, lcol, llab, acc1, pc1);
+      // the epilogue's streamed diagonal of the lane's first panel row, loaded before the accumulation
+      // so its HBM latency overlaps the gathers
+      float dga0 = 0.0f, dga1 = 0.0f;
+#if MGK_PANEL_DGPF
+      if (ra < rend) {
+        dga0 = ld_stream(DG + i * m + ra);
+        if (two) dga1 = ld_stream(DG + (i + 1) * m + ra);
+      }
+#endif
+      row_accumulate<NS, EK, LAP>(ek, v.ue, v.urp[i], v.urp[i + 1], lp, m, llab, acc0, pc0);
+      if (two) row_accumulate<NS, EK, LAP>(ek, v.ue, v.urp[i + 1], v.urp[i + 2], lp, m, llab, acc1, pc1);
 #pragma unroll
       for (int t = 0; t < NS; ++t) {
         SEG[lane + 32 * t] = acc0[t] * lw[t];
@@ -375,7 +408,8 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
         }
         const int e0 = base + r;
         const float p0 = P[e0];
-        const float a0 = fmaf(ld_stream(DG + e0), p0, -s0);
+        const bool pf = MGK_PANEL_DGPF && r == ra;
+        const float a0 = fmaf(pf ? dga0 : ld_stream(DG + e0), p0, -s0);
         AP[e0] = a0;
         if (part) {
           pap += (double)p0 * (double)a0;
@@ -383,7 +417,7 @@ __device__ void xmv_panels(const KernelDesc& ek, const PairView& v, const float*
         }
         if (two) {
           const float p1 = P[e0 + m];
-          const float a1 = fmaf(ld_stream(DG + e0 + m), p1, -s1);
+          const float a1 = fmaf(pf ? dga1 : ld_stream(DG + e0 + m), p1, -s1);
           AP[e0 + m] = a1;
           if (part) {
             pap += (double)p1 * (double)a1;
@@ -427,6 +461,13 @@ __device__ void xmv_panels_sym(const KernelDesc& ek, const PairView& v, const fl
       lkab[t] = kk.x | (kk.y << 16);
     }
   }
+  const float* lpa[NSU];
+  const float* lpb[NSU];
+#pragma unroll
+  for (int t = 0; t < NSU; ++t) {
+    lpa[t] = opaque_ptr(P + lca[t]);
+    lpb[t] = opaque_ptr(P + lcb[t]);
+  }
   const int ra = lane, rb = lane + 32;
   int qa0 = 0, qa1 = 0, qb0 = 0, qb1 = 0;
   float pla = 0.0f, plb = 0.0f;
@@ -455,11 +496,10 @@ __device__ void xmv_panels_sym(const KernelDesc& ek, const PairView& v, const fl
         int k = v.urp[i + r];
         for (; k + 1 < k1; k += 2) {
           const float4 e0 = v.ue[k], e1 = v.ue[k + 1];
-          const float* r0 = P + __float_as_int(e0.x) * m;
-          const float* r1 = P + __float_as_int(e1.x) * m;
+          const unsigned o0 = (unsigned)(__float_as_int(e0.x) * m), o1 = (unsigned)(__float_as_int(e1.x) * m);
 #pragma unroll
           for (int t = 0; t < NSU; ++t) {
-            const float x0a = r0[lca[t]], x0b = r0[lcb[t]], x1a = r1[lca[t]], x1b = r1[lcb[t]];
+            const float x0a = lpa[t][o0], x0b = lpb[t][o0], x1a = lpa[t][o1], x1b = lpb[t][o1];
             const float c0 = edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y);
             const float c1 = edge_kappa_w<EK>(ek, e1.z, llab[t], EK == KK_SE ? e1.w : e1.y);
             a[r][t] = fmaf(c0, x0a, a[r][t]);
@@ -470,12 +510,12 @@ __device__ void xmv_panels_sym(const KernelDesc& ek, const PairView& v, const fl
         }
         if (k < k1) {
           const float4 e0 = v.ue[k];
-          const float* r0 = P + __float_as_int(e0.x) * m;
+          const unsigned o0 = (unsigned)(__float_as_int(e0.x) * m);
 #pragma unroll
           for (int t = 0; t < NSU; ++t) {
             const float c0 = edge_kappa_w<EK>(ek, e0.z, llab[t], EK == KK_SE ? e0.w : e0.y);
-            a[r][t] = fmaf(c0, r0[lca[t]], a[r][t]);
-            b[r][t] = fmaf(c0, r0[lcb[t]], b[r][t]);
+            a[r][t] = fmaf(c0, lpa[t][o0], a[r][t]);
+            b[r][t] = fmaf(c0, lpb[t][o0], b[r][t]);
           }
         }
       }

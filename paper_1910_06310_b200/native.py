@@ -172,7 +172,7 @@ class Context:
         K = np.empty((G, G), dtype=np.float64)
         cv = np.empty((G, G), dtype=np.uint8)
         check(self.lib.mgk_gram(self.h, float(tol), int(max_iter), _ptr(K), None, _ptr(cv)))
-        it = np.empty((G, G), dtype=np.int64)  # widened on the device (GramResult.iterations is int64)
+        it = np.empty((G, G), dtype=np.int64)  # int32 over PCIe, widened by libmgk's host copy threads
         check(self.lib.mgk_gram_iterations64(self.h, _ptr(it)))
         return K, it, cv.view(bool)
 
