@@ -71,7 +71,15 @@ static void host_move(char* dst, const char* src, size_t bytes, bool widen, int 
 }
 
 cudaError_t d2h_staged(void* dst, const void* src, size_t bytes, bool widen = false) {
-  if (bytes < kStageMin && !widen) return d2h(dst, src, bytes);
+  if (bytes < kStageMin) {  // small results (config 1: a 16 x 16 Gram): one plain copy, no staging threads
+    if (!widen) return d2h(dst, src, bytes);
+    std::vector<int32_t> tmp(bytes / 4);
+    cudaError_t r = d2h(tmp.data(), src, bytes);
+    if (r != cudaSuccess) return r;
+    int64_t* d = static_cast<int64_t*>(dst);
+    for (size_t i = 0; i < tmp.size(); ++i) d[i] = tmp[i];
+    return cudaSuccess;
+  }
   g_d2h_bytes += (int64_t)bytes;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
