@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 for c in "$@"; do
   case $c in
-    1) args="--config 1 --steps 20 --warmup 5";;
+    1) args="--config 1 --steps 3000 --warmup 5";;  # >= 1 s timed region: the nvidia-smi clock sampler needs it
     3|5|5nw) args="--config $c --steps 2 --warmup 3";;
     *) args="--config $c --steps 1 --warmup 3";;
   esac
