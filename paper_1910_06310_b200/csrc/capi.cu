@@ -100,7 +100,8 @@ cudaError_t d2h_staged(void* dst, const void* src, size_t bytes, bool widen = fa
     if (e != cudaSuccess) return e;
     S.device = dev;
   }
-  const int threads = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  static const int max_threads = getenv("MGK_D2H_THREADS") ? std::max(1, atoi(getenv("MGK_D2H_THREADS"))) : 8;
+  const int threads = (int)std::max(1u, std::min((unsigned)max_threads, std::thread::hardware_concurrency()));
   const size_t nchunks = (bytes + kStageBytes - 1) / kStageBytes;
   auto issue = [&](size_t k) {
     const size_t off = k * kStageBytes, len = std::min(kStageBytes, bytes - off);
